@@ -1,0 +1,222 @@
+/*
+ * ectgpu — B200 (sm_100a) drop-in for the ectsim A–V assembly + Krylov hot path.
+ *
+ * C ABI only: plain pointers and sizes, no C++/torch types cross it. Complex
+ * arrays are interleaved (re, im) doubles = std::complex<double> /
+ * cuDoubleComplex layout. Every buffer argument may be HOST memory (copied
+ * through pinned staging) or DEVICE memory of the context's GPU (used in
+ * place); the library detects which with cudaPointerGetAttributes.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/core/...). Status codes mirror the reference's
+ * exception classes (types.hpp:53-64, exit codes ect_main.cpp:18-22):
+ *   0 ok, 2 ConfigError, 3 MeshError, 4 SolverError, 5 IoError,
+ *   6 CUDA/device error, 1 other. ect_last_error() returns the message of the
+ *   calling thread's last failure.
+ *
+ * Thread safety: a context owns one CUDA stream; calls on one context are
+ * serialised internally, so ScanSession-style concurrent callers
+ * (scan.cpp:155-156) are safe. Use one context per host thread for overlap.
+ */
+#ifndef ECTGPU_H_
+#define ECTGPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECT_OK 0
+#define ECT_ERR_OTHER 1
+#define ECT_ERR_CONFIG 2
+#define ECT_ERR_MESH 3
+#define ECT_ERR_SOLVER 4
+#define ECT_ERR_IO 5
+#define ECT_ERR_CUDA 6
+
+/* RegionTag (types.hpp:22-29). */
+#define ECT_REGION_TUBE 0
+#define ECT_REGION_TSP 1
+#define ECT_REGION_DEFECT 2
+#define ECT_REGION_COIL1 3
+#define ECT_REGION_COIL2 4
+#define ECT_REGION_VACUUM 5
+#define ECT_REGION_COUNT 6
+
+typedef struct ect_ctx ect_ctx;
+typedef struct ect_mesh ect_mesh;
+typedef struct ect_matrix ect_matrix;
+typedef struct ect_session ect_session;
+
+/* MaterialTable (materials.hpp:21-48), same field order. */
+typedef struct ect_materials {
+  double omega;
+  double sigma[ECT_REGION_COUNT];
+  double mu[ECT_REGION_COUNT];
+  double mu_tilde;
+  double delta_gauge;
+  double bc_penalty;
+  double sigma_eps;
+  int32_t ibc_enabled;       /* must be 0: IBC surface terms are out of scope */
+  int32_t l22_use_sigma_eps;
+} ect_materials;
+
+/* RunConfig [materials] keys (config.hpp:25-39). Negative sigma_defect /
+ * mu_r_defect mean "unset" (defaults to the tube values, config.cpp:333-334). */
+typedef struct ect_physics {
+  double frequency;
+  double sigma_tube;
+  double mu_r_tube;
+  double sigma_defect;
+  double mu_r_defect;
+  double sigma_eps_ratio;
+  double delta_gauge;
+  double bc_penalty;
+  int32_t mu_tilde_harmonic;
+  double mu_tilde_fixed;
+} ect_physics;
+
+/* CoilPair (tube_mesh.hpp:13-21). */
+typedef struct ect_coil {
+  double r_inner;
+  double r_outer;
+  double height;
+  double gap;
+} ect_coil;
+
+/* IterativeOptions (solver.hpp:54-58). max_iter counts Krylov iterations per
+ * right-hand side; restart is accepted for signature parity (COCG has none). */
+typedef struct ect_iter_options {
+  double tol;
+  int32_t max_iter;
+  int32_t restart;
+} ect_iter_options;
+
+/* IterativeResult (solver.hpp:60-65) minus x (written to the caller's buffer). */
+typedef struct ect_iter_result {
+  double residual;     /* true ||b - A x|| / ||b|| at exit */
+  int32_t iterations;
+  int32_t converged;
+} ect_iter_result;
+
+/* SignalPoint (signals.hpp:63-69). dz = {Z11, Z12, Z21, Z22} complex. */
+typedef struct ect_signal_point {
+  double z;
+  double dz[8];
+  double z_fa[2];
+  double z_f3[2];
+  int32_t failed;
+  int32_t iterations[4]; /* primary coil1, coil2, reference coil1, coil2 */
+} ect_signal_point;
+
+/* Per-phase device timings (ms, CUDA events) of the last call on a context. */
+typedef struct ect_timings {
+  double pattern_ms;
+  double assemble_ms;
+  double rhs_ms;
+  double solve_ms;
+  double spmv_ms_total;   /* sum of SpMV kernel durations inside the solve */
+  int64_t spmv_launches;
+  int64_t kernel_launches;
+} ect_timings;
+
+/* ---- context --------------------------------------------------------- */
+int ect_ctx_create(int device, ect_ctx** out);
+int ect_ctx_destroy(ect_ctx* ctx);
+const char* ect_last_error(void);
+int ect_ctx_timings(ect_ctx* ctx, ect_timings* out, int reset);
+/* Record per-launch SpMV events inside solves (adds two event records per
+ * iteration; used by bench.py for the roofline figure). */
+int ect_ctx_set_profiling(ect_ctx* ctx, int enabled);
+int ect_ctx_synchronize(ect_ctx* ctx);
+
+/* ---- mesh --------------------------------------------------------------
+ * Replaces Mesh construction + canonicalize_orientation (mesh.cpp:50-61),
+ * conductor_map (mesh.cpp:267-284) and the boundary classification that
+ * apply_essential_bc pins (mesh.cpp:145-182, assembly.cpp:285-312).
+ * tets: int32[n_tets*4] (reoriented in the device copy if negative),
+ * region: uint8 RegionTag per tet, xyz: double[n_nodes*3]. */
+int ect_mesh_create(ect_ctx* ctx, const double* xyz, int64_t n_nodes, const int32_t* tets,
+                    const uint8_t* region, int64_t n_tets, ect_mesh** out);
+int ect_mesh_destroy(ect_mesh* mesh);
+/* counts: n_nodes, n_tets, n_cond, n_dofs (3 n_nodes + n_cond), n_pins, n_defect_tets */
+int ect_mesh_counts(ect_mesh* mesh, int64_t counts[6]);
+/* ConductorIndexMap::forward (mesh.hpp:81-86), pinned A-dofs ascending
+ * (the std::set order of apply_essential_bc), canonical connectivity. */
+int ect_mesh_export(ect_mesh* mesh, int32_t* cond_forward, int32_t* pinned_dofs, int32_t* tets);
+
+/* ---- materials (host) ---------------------------------------------------
+ * RunConfig::material_table + resolve_mu_tilde (config.cpp:325-352),
+ * reference_variant (materials.cpp:44-53), and ScanSession's two-config rule
+ * (scan.cpp:46-49). */
+int ect_materials_from_physics(ect_mesh* mesh, const ect_physics* physics, ect_materials* primary,
+                               ect_materials* reference, int32_t* two_configs);
+/* harmonic_mu_tilde (materials.cpp:32-42), sequential in tet order. */
+int ect_harmonic_mu_tilde(ect_mesh* mesh, const ect_materials* mats, double* out);
+
+/* ---- matrix ------------------------------------------------------------
+ * K1: symbolic pattern == the CSC arrays CscMatrix::from_triplets produces
+ * for build_global (sparse.cpp:83-113, assembly.cpp:386-419). The pattern is
+ * structurally symmetric, so the CSR row_ptr/col_idx returned here are
+ * bit-identical to the reference's col_ptr/row_idx. */
+int ect_matrix_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix** out);
+/* Upload an external CSR (e.g. the oracle's) for SpMV/solve parity. */
+int ect_matrix_from_csr(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* row_ptr,
+                        const int32_t* col_idx, const double* values, ect_matrix** out);
+int ect_matrix_destroy(ect_matrix* m);
+int ect_matrix_counts(ect_matrix* m, int64_t* n, int64_t* nnz);
+/* K2: assemble_system + apply_essential_bc + build_global values
+ * (assembly.cpp:74-276, 285-327, 386-419). Deterministic, no fp64 atomics. */
+int ect_matrix_assemble(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* mats, ect_matrix* m);
+int ect_matrix_export(ect_matrix* m, int32_t* row_ptr, int32_t* col_idx, double* values);
+
+/* ---- right-hand sides ----------------------------------------------------
+ * K3: coil_support + assemble_rhs + apply_pins_to_rhs for n_rhs (probe z,
+ * coil) pairs (tube_mesh.cpp:272-288, assembly.cpp:329-378, scan.cpp:87-93).
+ * Output column r of an interleaved [n_dofs][n_rhs] complex array. */
+int ect_rhs_coil(ect_ctx* ctx, ect_mesh* mesh, const ect_coil* coil, const double* probe_z,
+                 const int32_t* which_coil, int32_t n_rhs, double amplitude, double* rhs);
+
+/* ---- SpMV / solve --------------------------------------------------------
+ * K4: y = A x (CscMatrix::multiply, sparse.cpp:115-124) for n_rhs vectors in
+ * interleaved [n][n_rhs] layout. */
+int ect_spmv(ect_ctx* ctx, ect_matrix* m, const double* x, double* y, int32_t n_rhs);
+/* K5/K6: solve_iterative (iterative.cpp:109-228) replacement: Jacobi-
+ * preconditioned COCG (A is complex symmetric) for n_rhs right-hand sides
+ * sharing one matrix pass per iteration; true-residual confirmation as
+ * iterative.cpp:208-216. b, x interleaved [n][n_rhs]. Non-convergence is
+ * reported in results (not an error), breakdown returns ECT_ERR_SOLVER. */
+int ect_solve(ect_ctx* ctx, ect_matrix* m, const double* b, double* x, int32_t n_rhs,
+              const ect_iter_options* opts, ect_iter_result* results);
+
+/* ---- impedance ----------------------------------------------------------
+ * K7: delta_impedance over DEFECT tets for the four (k, l) pairings of
+ * primary solutions x_k (k=1,2) and reference solutions x_l (l=1,2)
+ * (signals.cpp:67-99, scan.cpp:123-135). xs: 4 device-or-host vectors
+ * [x_k1, x_k2, x_l1, x_l2], each n_dofs complex. dz: 8 doubles. */
+int ect_delta_impedance(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* primary,
+                        const ect_materials* reference, const double* x_k1, const double* x_k2,
+                        const double* x_l1, const double* x_l2, double* dz);
+
+/* ---- scan session (ScanSession, scan.hpp:39-72) ---------------------------
+ * Assembles the primary (+ reference) matrix once; solve_positions runs
+ * solve_position (scan.cpp:95-143) for each z with the coil pair's two
+ * right-hand sides batched into one COCG per material configuration. */
+int ect_session_create(ect_ctx* ctx, ect_mesh* mesh, const ect_physics* physics,
+                       const ect_coil* coil, double amplitude, const ect_iter_options* opts,
+                       ect_session** out);
+int ect_session_destroy(ect_session* s);
+int ect_session_matrix(ect_session* s, int reference, ect_matrix** out);
+/* positions_per_batch: probe positions whose 2*P right-hand sides share one
+ * matrix pass (1..8). solutions: optional host/device buffer receiving the
+ * 4 solution vectors of the LAST position ([4][n_dofs] complex) or NULL. */
+int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
+                                int32_t positions_per_batch, ect_signal_point* out,
+                                double* solutions);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECTGPU_H_ */

@@ -1,0 +1,156 @@
+"""Generate the golden fixtures in tests/golden/ from the reference build.
+
+TEST INFRASTRUCTURE. Runs the UNMODIFIED reference core (oracle/_ref,
+built by oracle/Makefile from /root/reference) on the synthetic box meshes and
+stores what it produces, so the GPU box (which has no /root/reference) can
+check parity against committed data:
+
+  small_*.npz    full arrays for small meshes: cond map, pins, CSC arrays,
+                 values, coil right-hand sides, DIRECT-LU solutions
+                 (Factorization, solver.cpp:197-376) for both material
+                 configurations, DeltaZ and the signal modes.
+  cfg0.npz       configs[0]: sha256 of the CSC pattern / values, counts,
+                 right-hand sides and GMRES(80)+ILU(0) solutions at tol 1e-12.
+  cfg1.json      configs[1]: counts + sha256 of the CSC pattern and values
+                 (reference assembly takes minutes and ~20 GB; run once).
+
+usage: python -m oracle.make_golden [small|cfg0|cfg1|all]
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+from oracle import ref
+from paper_1602_03207_b200 import workloads
+
+GOLDEN = Path(__file__).resolve().parent.parent / "tests" / "golden"
+
+SMALL_CASES = {
+    "small_4x4x8": dict(n=(4, 4, 8), seed=7, deposit=True),
+    "small_6x6x12": dict(n=(6, 6, 12), seed=3, deposit=True),
+    "small_5x5x10_nodefect": dict(n=(5, 5, 10), seed=11, deposit=False),
+}
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def mats_to_array(m: ref.Materials) -> np.ndarray:
+    return np.array([m.omega, *m.sigma, *m.mu, m.mu_tilde, m.delta_gauge, m.bc_penalty,
+                     m.sigma_eps, m.ibc_enabled, m.l22_use_sigma_eps], dtype=np.float64)
+
+
+def reference_case(w, direct=True, tol=1e-12):
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    ex = rm.export()
+    assert np.array_equal(ex["tets"], mesh.tets), "generator tets are not canonical"
+    prim, refm, two = rm.materials(w.physics)
+    out = {"xyz": mesh.xyz, "tets": mesh.tets, "region": mesh.region,
+           "cond_forward": ex["cond_forward"], "two_configs": np.array(two),
+           "mats_primary": mats_to_array(prim), "mats_reference": mats_to_array(refm),
+           "coil": np.array(w.coil), "z": np.array(w.positions[0]),
+           "amplitude": np.array(w.amplitude)}
+    systems = [("primary", prim)] + ([("reference", refm)] if two else [])
+    t0 = time.time()
+    for tag, mats in systems:
+        s = ref.RefSystem(rm, mats, parts=1, workers=1)
+        col_ptr, row_idx, vals, pins = s.export()
+        out[f"{tag}_col_ptr"] = col_ptr
+        out[f"{tag}_row_idx"] = row_idx
+        out[f"{tag}_values"] = vals
+        out["pins"] = np.sort(pins)
+        if tag == "primary":
+            b = np.stack([s.position_rhs(w.coil, w.positions[0], c, w.amplitude) for c in (1, 2)])
+            out["rhs"] = b
+        if direct:
+            x, res = s.solve_direct(out["rhs"])
+        else:
+            x = np.empty_like(out["rhs"])
+            res = np.empty(2)
+            for c in range(2):
+                r = s.solve_iterative(out["rhs"][c], tol=tol, max_iter=20000, restart=150)
+                assert r["converged"], r
+                x[c], res[c] = r["x"], r["residual"]
+        out[f"{tag}_x"] = x
+        out[f"{tag}_residual"] = res
+    if two:
+        dz = np.array([rm.delta_impedance(prim, refm, out["primary_x"][k], out["reference_x"][l])
+                       for k in range(2) for l in range(2)])
+        out["dz"] = dz
+        out["modes"] = np.array(ref.signal_modes(dz))
+    print(f"{w.name}: N={len(out['primary_col_ptr']) - 1} nnz={len(out['primary_row_idx'])} "
+          f"pins={len(out['pins'])} two={two} ({time.time() - t0:.1f}s)")
+    return out
+
+
+def make_small():
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    for name, kw in SMALL_CASES.items():
+        w = workloads.small(**kw)
+        out = reference_case(w, direct=True)
+        np.savez_compressed(GOLDEN / f"{name}.npz", **out)
+
+
+def make_cfg0():
+    w = workloads.config0()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    s = ref.RefSystem(rm, prim, parts=1, workers=1)
+    col_ptr, row_idx, vals, pins = s.export()
+    b = np.stack([s.position_rhs(w.coil, w.positions[0], c, w.amplitude) for c in (1, 2)])
+    xs, its, res = [], [], []
+    for c in range(2):
+        r = s.solve_iterative(b[c], tol=1e-12, max_iter=20000, restart=150)
+        assert r["converged"], r
+        xs.append(r["x"])
+        its.append(r["iterations"])
+        res.append(r["residual"])
+        print(f"cfg0 coil {c + 1}: GMRES iterations {r['iterations']} residual {r['residual']:.3e}"
+              f" in {r['seconds']:.1f}s")
+    np.savez_compressed(
+        GOLDEN / "cfg0.npz", n=len(col_ptr) - 1, nnz=len(row_idx), n_pins=len(pins),
+        sha_col_ptr=sha(col_ptr), sha_row_idx=sha(row_idx), sha_values=sha(vals),
+        cond_forward_sha=sha(rm.export()["cond_forward"]), pins_sha=sha(np.sort(pins)),
+        mats_primary=mats_to_array(prim), rhs=b, x=np.stack(xs), gmres_iterations=np.array(its),
+        gmres_residual=np.array(res), frob=np.linalg.norm(vals),
+        timings=np.array([s.timings[k] for k in ("assemble", "reduce", "bc", "build_global")]))
+
+
+def make_cfg1():
+    w = workloads.config1()
+    t0 = time.time()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    out = {"n_nodes": rm.n_nodes, "n_tets": rm.n_tets, "n_cond": rm.n_cond, "two_configs": two,
+           "mu_tilde": prim.mu_tilde, "cond_forward_sha": sha(rm.export()["cond_forward"])}
+    for tag, mats in (("primary", prim), ("reference", refm)):
+        s = ref.RefSystem(rm, mats, parts=8, workers=8)
+        col_ptr, row_idx, vals, pins = s.export()
+        out[tag] = {"n": int(len(col_ptr) - 1), "nnz": int(len(row_idx)), "n_pins": int(len(pins)),
+                    "sha_col_ptr": sha(col_ptr), "sha_row_idx": sha(row_idx),
+                    "frob": float(np.linalg.norm(vals)),
+                    "timings_s": {k: float(v) for k, v in s.timings.items()}}
+        out["pins_sha"] = sha(np.sort(pins))
+        del s, col_ptr, row_idx, vals
+        print(tag, out[tag], f"{time.time() - t0:.0f}s", flush=True)
+    (GOLDEN / "cfg1.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "small"
+    if what in ("small", "all"):
+        make_small()
+    if what in ("cfg0", "all"):
+        make_cfg0()
+    if what in ("cfg1", "all"):
+        make_cfg1()

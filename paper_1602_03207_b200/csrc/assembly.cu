@@ -1,0 +1,264 @@
+// K2: numeric assembly of the A–V matrix, fused with the essential-BC pins.
+//
+// Replaces assemble_system (assembly.cpp:243-276) -> assemble_block
+// (assembly.cpp:74-235) -> reduce_blocks/canonicalize (sparse.cpp:13-57) ->
+// apply_essential_bc/apply_pins_to_matrix (assembly.cpp:285-327) ->
+// build_global/from_triplets (assembly.cpp:386-419, sparse.cpp:83-113).
+//
+// B200 design — row-owner gather, no fp64 atomics, no triplets:
+//   * one warp per mesh node i owns the 3 A-rows of i and its V-row;
+//   * lane r owns neighbour m_r (from K1's neighbour list), i.e. the 3x3
+//     A-A block (3i+c, 3m_r+d), the A-V column, the V-A row and the V-V entry;
+//   * the warp walks i's incident tets in ascending tet id (the reference's
+//     insertion order with one partition), each lane computing one tet frame
+//     per 32-tet chunk into shared memory; every lane then adds the local
+//     entry (a_i, b_{m_r}) of each tet containing m_r — so every CSR slot is
+//     a left fold over tets in exactly the reference's order, written once.
+//   * compiled with -fmad=false: element arithmetic is the reference's IEEE
+//     sequence (elements.cuh), making the values bit-identical to the oracle.
+// Bytes: coords/connectivity gathers (L2-resident) + one write of each value.
+#include <cub/cub.cuh>
+
+#include "elements.cuh"
+#include "ect_internal.h"
+
+namespace ect {
+namespace {
+
+constexpr int kWarps = 8;  // warps per block
+
+__device__ __forceinline__ bool is_conductor(uint8_t r) {
+  return r == ECT_REGION_TUBE || r == ECT_REGION_TSP || r == ECT_REGION_DEFECT;
+}
+
+struct AsmParams {
+  RegionCoef coef[ECT_REGION_COUNT];
+  double bc_penalty;
+  int l22_eps;  // MaterialTable::l22_use_sigma_eps
+};
+
+struct TetSlot {
+  double g[4][3];
+  double vol;
+  int nodes[4];
+  int region;
+  int a;  // local index of the owning node
+};
+
+__global__ void __launch_bounds__(kWarps * 32)
+k_assemble(const int4* __restrict__ tets, const uint8_t* __restrict__ region,
+           const double* __restrict__ xyz, const int* __restrict__ inc_off,
+           const int* __restrict__ inc, const int* __restrict__ nbr_off,
+           const int* __restrict__ nbr, const uint8_t* __restrict__ nbr_cond,
+           const int* __restrict__ cond_fwd, const uint8_t* __restrict__ pinned,
+           const int* __restrict__ row_ptr, int64_t n_nodes, AsmParams P, double2* val,
+           int* err) {
+  __shared__ TetSlot slots[kWarps][32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  TetSlot* my = slots[wib];
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int na = (int)(3 * n_nodes);
+
+  for (int64_t i = warp; i < n_nodes; i += n_warps) {
+    const int ib = inc_off[i], deg = inc_off[i + 1] - ib;
+    const int nb = nbr_off[i], u = nbr_off[i + 1] - nb;
+    int ncc = 0;
+    for (int r0 = 0; r0 < u; r0 += 32) {
+      bool c = (r0 + lane < u) && nbr_cond[nb + r0 + lane];
+      ncc += __popc(__ballot_sync(0xffffffffu, c));
+    }
+    const int cf_i = cond_fwd[i];
+    int rc0 = 0;
+    for (int r0 = 0; r0 < u; r0 += 32) {
+      const int r = r0 + lane;
+      const bool valid = r < u;
+      const int m = valid ? nbr[nb + r] : -1;
+      const bool mc = valid && nbr_cond[nb + r];
+      const unsigned cmask = __ballot_sync(0xffffffffu, mc);
+      const int rc = rc0 + __popc(cmask & ((1u << lane) - 1u));
+      rc0 += __popc(cmask);
+
+      double aa[3][3];     // A-A real parts
+      double aa_im[3];     // imaginary parts live on c == d only
+      double av[3], va[3];  // couplings are real (element_forms.cpp:75-99)
+      double vv_re = 0.0, vv_im = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        aa_im[c] = 0.0;
+        av[c] = 0.0;
+        va[c] = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) aa[c][d] = 0.0;
+      }
+      bool seen = false, seen_c = false;
+
+      for (int t0 = 0; t0 < deg; t0 += 32) {
+        const int cnt = min(32, deg - t0);
+        __syncwarp();
+        if (lane < cnt) {
+          const int e = inc[ib + t0 + lane];
+          const int t = e >> 2;
+          const int4 k = tets[t];
+          TetSlot& S = my[lane];
+          S.nodes[0] = k.x;
+          S.nodes[1] = k.y;
+          S.nodes[2] = k.z;
+          S.nodes[3] = k.w;
+          S.region = region[t];
+          S.a = e & 3;
+          double p[4][3];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p[q][c] = xyz[3 * (int64_t)S.nodes[q] + c];
+          TetGeom f;
+          tet_frame(p, f);
+          if (!f.ok) atomicOr(err, 1);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) S.g[q][c] = f.g[q][c];
+          S.vol = f.vol;
+        }
+        __syncwarp();
+        if (valid) {
+          for (int q = 0; q < cnt; ++q) {
+            const TetSlot& S = my[q];
+            const int b = S.nodes[0] == m ? 0 : S.nodes[1] == m ? 1 : S.nodes[2] == m ? 2
+                                                                : S.nodes[3] == m ? 3 : -1;
+            if (b < 0) continue;
+            const int a = S.a;
+            const RegionCoef& C = P.coef[S.region];
+            const double vol = S.vol;
+            double ga[3], gb[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              ga[c] = S.g[a][c];
+              gb[c] = S.g[b][c];
+            }
+            // element_l11 (element_forms.cpp:49-73)
+            const double dot = dot3(ga, gb);
+            const double mass = (vol * (a == b ? 2.0 : 1.0)) / 20.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                const double curl = (c == d ? dot : 0.0) - ga[d] * gb[c];
+                double value = vol * (C.mu_inv * curl + (C.mt_inv * ga[c]) * gb[d]);
+                if (c == d) value = value + 0.0;  // complexd += (0*mass, ...)
+                aa[c][d] = seen ? aa[c][d] + value : value;
+              }
+              const double im = 0.0 + C.mass_im * mass;
+              aa_im[c] = seen ? aa_im[c] + im : im;
+            }
+            seen = true;
+            if (is_conductor((uint8_t)S.region)) {
+              const double w = vol / 4.0;
+              // element_l12 (3a+c, b) and element_l21 (a, 3b+d)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                const double x12 = (C.neg_sigma * gb[c]) * w;
+                const double x21 = (C.neg_sigma * ga[c]) * w;
+                av[c] = seen_c ? av[c] + x12 : x12;
+                va[c] = seen_c ? va[c] + x21 : x21;
+              }
+              // element_l22 (element_forms.cpp:101-114) [+ l22_use_sigma_eps branch,
+              // assembly.cpp:147-158]
+              const double s = vol * dot;
+              double re, imv;
+              if (!P.l22_eps) {
+                re = (0.0 * s) + C.gauge * mass;
+                imv = C.stiff_im * s;
+              } else {
+                const double g_re = ((0.0 * s) + C.gauge * mass) - ((0.0 * s) + 0.0 * mass);
+                const double g_im = C.stiff_im * s - C.stiff_im * s;
+                re = ((0.0 * s) + 0.0 * mass) + g_re;
+                imv = C.stiff_im_eps * s + g_im;
+              }
+              vv_re = seen_c ? vv_re + re : re;
+              vv_im = seen_c ? vv_im + imv : imv;
+              seen_c = true;
+            }
+          }
+        }
+      }
+
+      if (valid) {
+        // apply_pins_to_matrix: overwrite the pinned diagonal (assembly.cpp:314-327)
+        if (m == (int)i) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (pinned[3 * i + c]) {
+              aa[c][c] = P.bc_penalty;
+              aa_im[c] = 0.0;
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int base = row_ptr[3 * i + c];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            val[base + 3 * r + d] = make_double2(aa[c][d], c == d ? aa_im[c] : 0.0);
+          }
+          if (mc) val[base + 3 * u + rc] = make_double2(av[c], 0.0);
+        }
+        if (mc && cf_i >= 0) {
+          const int basev = row_ptr[na + cf_i];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) val[basev + 3 * rc + d] = make_double2(va[d], 0.0);
+          val[basev + 3 * ncc + rc] = make_double2(vv_re, vv_im);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a) {
+  ect_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  if (mats.ibc_enabled) {
+    fail(ECT_ERR_CONFIG, "impedance boundary condition (ibc_enabled) is not supported by the GPU path");
+  }
+  if (!a->from_mesh || a->n_nodes != m->n_nodes) {
+    fail(ECT_ERR_SOLVER, "assemble: matrix pattern was not built from this mesh");
+  }
+  AsmParams P{};
+  for (int r = 0; r < ECT_REGION_COUNT; ++r) {
+    RegionCoef& C = P.coef[r];
+    const double sigma = mats.sigma[r], mu = mats.mu[r];
+    C.mu_inv = 1.0 / mu;
+    C.mt_inv = 1.0 / mats.mu_tilde;
+    C.mass_im = (-1.0 * mats.omega) * sigma;
+    C.sigma = sigma;
+    C.neg_sigma = -sigma;
+    C.stiff_im = sigma / mats.omega;
+    C.gauge = (mats.delta_gauge * mu) * sigma;
+    C.stiff_im_eps = mats.sigma_eps / mats.omega;
+  }
+  P.bc_penalty = mats.bc_penalty;
+  P.l22_eps = mats.l22_use_sigma_eps;
+  DevBuf<int> err(1);
+  CK(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+  int64_t blocks = (m->n_nodes + kWarps - 1) / kWarps;
+  int64_t cap = (int64_t)ctx->num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  k_assemble<<<(int)blocks, kWarps * 32, 0, s>>>(m->tets.p, m->region.p, m->xyz.p, m->inc_off.p,
+                                                m->inc.p, m->nbr_off.p, m->nbr.p, m->nbr_cond.p,
+                                                m->cond_fwd.p, m->pinned.p, a->row_ptr.p,
+                                                m->n_nodes, P, a->val.p, err.p);
+  CK_LAUNCH();
+  note_launch(ctx, 1);
+  int h_err = 0;
+  CK(cudaMemcpyAsync(&h_err, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h_err) fail(ECT_ERR_MESH, "element frame on a degenerate or inverted tet");
+  a->assembled = true;
+  compute_jacobi(a);
+}
+
+}  // namespace ect

@@ -1,0 +1,168 @@
+// Internal types shared by the ectgpu translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ectgpu.h"
+
+namespace ect {
+
+// Error carrying an ABI status code; thrown inside the library, converted to
+// a status at the C boundary (mirrors the reference's exception classes,
+// types.hpp:53-64).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& what) { throw Error(code, what); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    fail(ECT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                           std::to_string(line) + ")");
+  }
+}
+#define CK(x) ::ect::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::ect::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Owning device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Device-side per-right-hand-side Krylov state (see krylov.cu).
+struct RhsState {
+  double2 rho;    // r^T z (unconjugated, COCG)
+  double2 alpha;
+  double2 beta;
+  double bnorm;
+  double rnorm;
+  int iters;
+  int status;     // kActive / kConverged / kBreakdown / kMaxIter / kZeroRhs
+};
+enum RhsStatus : int { kActive = 0, kConverged = 1, kBreakdown = 2, kMaxIter = 3, kZeroRhs = 4 };
+
+// Per-context kernel accounting and optional SpMV event profiling.
+struct Profile {
+  bool enabled = false;
+  std::vector<cudaEvent_t> pool;  // pairs (start, stop)
+  size_t used = 0;
+  int64_t launches = 0;
+};
+
+}  // namespace ect
+
+struct ect_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::recursive_mutex mu;
+  ect::DevBuf<char> cub_tmp;
+  ect_timings timings{};
+  ect::Profile prof;
+  // pinned staging for host<->device copies
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  int* pinned_flag = nullptr;  // small pinned word for convergence polling
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+};
+
+struct ect_mesh {
+  ect_ctx* ctx = nullptr;
+  int64_t n_nodes = 0, n_tets = 0, n_cond = 0, n_pins = 0, n_defect = 0;
+  ect::DevBuf<double> xyz;         // [n_nodes][3]
+  ect::DevBuf<int4> tets;          // canonical connectivity
+  ect::DevBuf<uint8_t> region;     // RegionTag per tet
+  ect::DevBuf<int> cond_fwd;       // node -> conductor dof or -1
+  ect::DevBuf<int> inc_off;        // node -> incident tet range (n_nodes + 1)
+  ect::DevBuf<int> inc;            // 4 * tet + local index, ascending tet per node
+  ect::DevBuf<uint8_t> pinned;     // per A-dof (3 n_nodes) essential-BC flag
+  ect::DevBuf<int> defect_tets;    // DEFECT tets ascending (signals.cpp:67-99)
+  // node-neighbour structure produced by the pattern build (K1)
+  ect::DevBuf<int> nbr_off;        // n_nodes + 1
+  ect::DevBuf<int> nbr;            // neighbour node ids ascending, incl. self
+  ect::DevBuf<uint8_t> nbr_cond;   // neighbour shares a conductor tet
+  bool have_nbr = false;
+  // host copies (host-side reference semantics: mu_tilde, z extremes)
+  std::vector<double> h_xyz;
+  std::vector<int32_t> h_tets;
+  std::vector<uint8_t> h_region;
+  double z_lo = 0.0, z_hi = 0.0;
+  int max_inc = 0, max_nbr = 0;
+};
+
+struct ect_matrix {
+  ect_ctx* ctx = nullptr;
+  int64_t n = 0, nnz = 0;
+  int64_t n_nodes = 0, n_cond = 0;  // DOF structure when built from a mesh
+  bool from_mesh = false;
+  bool assembled = false;
+  ect::DevBuf<int> row_ptr;
+  ect::DevBuf<int> col;
+  ect::DevBuf<double2> val;
+  ect::DevBuf<double2> dinv;       // Jacobi preconditioner 1/diag
+};
+
+namespace ect {
+
+// Buffer argument that may be host or device memory.
+bool is_device_ptr(const void* p);
+
+// Kernel entry points implemented in the .cu files.
+void build_mesh_topology(ect_mesh* m);                         // mesh.cu
+void build_pattern(ect_mesh* m, ect_matrix* a);                // pattern.cu
+void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a);  // assembly.cu
+void compute_jacobi(ect_matrix* a);                            // krylov.cu
+void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k);  // spmv.cu
+void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* which, int n_rhs,
+               double amplitude, double2* rhs);                // rhs.cu
+void delta_impedance(ect_mesh* m, const ect_materials& p, const ect_materials& r,
+                     const double2* xk1, const double2* xk2, const double2* xl1,
+                     const double2* xl2, int stride, double2 out[4]);  // signals.cu
+struct SolveOut {
+  std::vector<int> iters;
+  std::vector<double> residual;
+  std::vector<int> converged;
+};
+void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
+                const ect_iter_options& opt, SolveOut* out);  // krylov.cu
+
+// cub temporary storage helper
+void* cub_scratch(ect_ctx* ctx, size_t bytes);
+int grid_for(ect_ctx* ctx, const void* kernel, int block, size_t smem = 0);
+void note_launch(ect_ctx* ctx, int n = 1);
+
+}  // namespace ect

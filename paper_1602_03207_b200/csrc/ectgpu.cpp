@@ -1,0 +1,706 @@
+// ectgpu C ABI (include/ectgpu.h) and the host-side mirror of the reference
+// API around it: mesh preparation, MaterialTable construction, ScanSession.
+//
+// Host arithmetic that defines matrix values (mu_tilde, material
+// coefficients) follows the reference sequentially and is compiled with
+// -ffp-contract=off, exactly like the reference on x86-64.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "ect_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+constexpr double kMu0 = 1.25663706212e-6;  // types.hpp:18
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ECT_OK;
+  } catch (const ect::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ECT_ERR_OTHER;
+  }
+}
+
+void require(bool ok, int code, const char* what) {
+  if (!ok) ect::fail(code, what);
+}
+
+// Input buffer that may live on the host or on the context's device.
+template <typename T>
+struct In {
+  const T* dev = nullptr;
+  ect::DevBuf<T> tmp;
+  In(ect_ctx* ctx, const T* p, size_t count) {
+    if (count == 0 || ect::is_device_ptr(p)) {
+      dev = p;
+      return;
+    }
+    tmp.alloc(count);
+    CK(cudaMemcpyAsync(tmp.p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    dev = tmp.p;
+  }
+};
+
+// Output buffer that may live on the host or on the device.
+template <typename T>
+struct Out {
+  T* dev = nullptr;
+  T* host = nullptr;
+  size_t count = 0;
+  ect::DevBuf<T> tmp;
+  ect_ctx* ctx;
+  Out(ect_ctx* c, T* p, size_t n) : count(n), ctx(c) {
+    if (n == 0 || ect::is_device_ptr(p)) {
+      dev = p;
+      return;
+    }
+    host = p;
+    tmp.alloc(n);
+    dev = tmp.p;
+  }
+  void finish() {
+    if (host) CK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+};
+
+struct ScopedDevice {
+  int prev = 0;
+  explicit ScopedDevice(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) CK(cudaSetDevice(d));
+  }
+  ~ScopedDevice() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct EventTimer {
+  ect_ctx* ctx;
+  double* slot;
+  EventTimer(ect_ctx* c, double* s) : ctx(c), slot(s) { CK(cudaEventRecord(ctx->ev_a, ctx->stream)); }
+  ~EventTimer() {
+    if (cudaEventRecord(ctx->ev_b, ctx->stream) != cudaSuccess) return;
+    if (cudaEventSynchronize(ctx->ev_b) != cudaSuccess) return;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b) == cudaSuccess) *slot += ms;
+  }
+};
+
+// signed_tet_volume (mesh.cpp:36-38) with the shim's cross/dot order.
+double signed_volume_host(const double* a, const double* b, const double* c, const double* d) {
+  const double u0 = b[0] - a[0], u1 = b[1] - a[1], u2 = b[2] - a[2];
+  const double v0 = c[0] - a[0], v1 = c[1] - a[1], v2 = c[2] - a[2];
+  const double w0 = d[0] - a[0], w1 = d[1] - a[1], w2 = d[2] - a[2];
+  const double cx = u1 * v2 - u2 * v1, cy = u2 * v0 - u0 * v2, cz = u0 * v1 - u1 * v0;
+  return ((cx * w0 + cy * w1) + cz * w2) / 6.0;
+}
+
+bool same_coefficients(const ect_materials& a, const ect_materials& b) {
+  // MaterialTable::same_coefficients (materials.cpp:24-30)
+  if (a.omega != b.omega || a.mu_tilde != b.mu_tilde || a.delta_gauge != b.delta_gauge ||
+      a.bc_penalty != b.bc_penalty || a.sigma_eps != b.sigma_eps ||
+      a.ibc_enabled != b.ibc_enabled || a.l22_use_sigma_eps != b.l22_use_sigma_eps)
+    return false;
+  for (int r = 0; r < ECT_REGION_COUNT; ++r)
+    if (a.sigma[r] != b.sigma[r] || a.mu[r] != b.mu[r]) return false;
+  return true;
+}
+
+void check_materials(const ect_materials& m) {
+  if (m.ibc_enabled) {
+    ect::fail(ECT_ERR_CONFIG,
+              "ibc_enabled: impedance surface terms are not supported by the GPU path");
+  }
+  require(m.omega > 0.0, ECT_ERR_CONFIG, "materials: omega must be positive");
+  require(m.mu_tilde > 0.0, ECT_ERR_CONFIG, "materials: mu_tilde must be positive");
+}
+
+}  // namespace
+
+namespace ect {
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr{};
+  cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+void* cub_scratch(ect_ctx* ctx, size_t bytes) {
+  ctx->cub_tmp.ensure(std::max<size_t>(bytes, 1));
+  return ctx->cub_tmp.p;
+}
+
+int grid_for(ect_ctx* ctx, const void* kernel, int block, size_t smem) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem));
+  return std::max(1, per_sm) * ctx->num_sms;
+}
+
+void note_launch(ect_ctx* ctx, int n) { ctx->timings.kernel_launches += n; }
+
+}  // namespace ect
+
+// ============================================================================
+extern "C" {
+
+const char* ect_last_error(void) { return g_last_error.c_str(); }
+
+int ect_ctx_create(int device, ect_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, ECT_ERR_OTHER, "ect_ctx_create: null output");
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    require(device >= 0 && device < count, ECT_ERR_CUDA, "ect_ctx_create: no such CUDA device");
+    auto ctx = std::make_unique<ect_ctx>();
+    ctx->device = device;
+    ScopedDevice sd(device);
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+      ect::fail(ECT_ERR_CUDA, std::string("ectgpu is built for sm_100a (B200); device is ") +
+                                  prop.name);
+    }
+    ctx->num_sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev_a));
+    CK(cudaEventCreate(&ctx->ev_b));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pinned_flag), 64, cudaHostAllocDefault));
+    *out = ctx.release();
+  });
+}
+
+int ect_ctx_destroy(ect_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    ScopedDevice sd(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto e : ctx->prof.pool) cudaEventDestroy(e);
+    if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
+    cudaEventDestroy(ctx->ev_a);
+    cudaEventDestroy(ctx->ev_b);
+    ctx->cub_tmp.release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int ect_ctx_timings(ect_ctx* ctx, ect_timings* out, int reset) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (out) *out = ctx->timings;
+    if (reset) ctx->timings = ect_timings{};
+  });
+}
+
+int ect_ctx_set_profiling(ect_ctx* ctx, int enabled) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx->prof.enabled = enabled != 0;
+  });
+}
+
+int ect_ctx_synchronize(ect_ctx* ctx) {
+  return guarded([&] {
+    ScopedDevice sd(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---- mesh ------------------------------------------------------------------
+int ect_mesh_create(ect_ctx* ctx, const double* xyz, int64_t n_nodes, const int32_t* tets,
+                    const uint8_t* region, int64_t n_tets, ect_mesh** out) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(n_nodes > 0 && n_tets > 0, ECT_ERR_MESH, "mesh: empty node or tet set");
+    auto m = std::make_unique<ect_mesh>();
+    m->ctx = ctx;
+    m->n_nodes = n_nodes;
+    m->n_tets = n_tets;
+    // Host copies; they also define mu_tilde and the z extremes exactly as
+    // the reference computes them. Pointers may be device memory.
+    m->h_xyz.resize(3 * n_nodes);
+    m->h_tets.resize(4 * n_tets);
+    m->h_region.resize(n_tets);
+    CK(cudaMemcpy(m->h_xyz.data(), xyz, 3 * n_nodes * sizeof(double), cudaMemcpyDefault));
+    CK(cudaMemcpy(m->h_tets.data(), tets, 4 * n_tets * sizeof(int32_t), cudaMemcpyDefault));
+    CK(cudaMemcpy(m->h_region.data(), region, n_tets, cudaMemcpyDefault));
+    for (int64_t t = 0; t < n_tets; ++t) {
+      int32_t* k = &m->h_tets[4 * t];
+      for (int a = 0; a < 4; ++a) {
+        if (k[a] < 0 || k[a] >= n_nodes) {
+          ect::fail(ECT_ERR_MESH, "tet " + std::to_string(t) + " references invalid node " +
+                                      std::to_string(k[a]));
+        }
+      }
+      if (m->h_region[t] >= ECT_REGION_COUNT) {
+        ect::fail(ECT_ERR_MESH, "tet " + std::to_string(t) + " carries unknown region tag");
+      }
+      // Mesh::canonicalize_orientation (mesh.cpp:50-61)
+      double vol = signed_volume_host(&m->h_xyz[3 * k[0]], &m->h_xyz[3 * k[1]],
+                                      &m->h_xyz[3 * k[2]], &m->h_xyz[3 * k[3]]);
+      if (vol < 0.0) {
+        std::swap(k[2], k[3]);
+        vol = -vol;
+      }
+      if (!(vol > 0.0)) {
+        ect::fail(ECT_ERR_MESH, "degenerate tet " + std::to_string(t) + " (zero volume)");
+      }
+    }
+    // classify_boundary's z extremes (mesh.cpp:146-153)
+    m->z_lo = m->z_hi = m->h_xyz[2];
+    for (int64_t i = 0; i < n_nodes; ++i) {
+      m->z_lo = std::min(m->z_lo, m->h_xyz[3 * i + 2]);
+      m->z_hi = std::max(m->z_hi, m->h_xyz[3 * i + 2]);
+    }
+    m->xyz.alloc(3 * n_nodes);
+    m->tets.alloc(n_tets);
+    m->region.alloc(n_tets);
+    CK(cudaMemcpyAsync(m->xyz.p, m->h_xyz.data(), m->xyz.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(m->tets.p, m->h_tets.data(), m->tets.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(m->region.p, m->h_region.data(), m->region.bytes(), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    ect::build_mesh_topology(m.get());
+    *out = m.release();
+  });
+}
+
+int ect_mesh_destroy(ect_mesh* mesh) {
+  return guarded([&] {
+    if (!mesh) return;
+    ScopedDevice sd(mesh->ctx->device);
+    delete mesh;
+  });
+}
+
+int ect_mesh_counts(ect_mesh* m, int64_t counts[6]) {
+  return guarded([&] {
+    counts[0] = m->n_nodes;
+    counts[1] = m->n_tets;
+    counts[2] = m->n_cond;
+    counts[3] = 3 * m->n_nodes + m->n_cond;
+    counts[4] = m->n_pins;
+    counts[5] = m->n_defect;
+  });
+}
+
+int ect_mesh_export(ect_mesh* m, int32_t* cond_forward, int32_t* pinned_dofs, int32_t* tets) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(m->ctx->mu);
+    ScopedDevice sd(m->ctx->device);
+    cudaStream_t s = m->ctx->stream;
+    if (cond_forward) {
+      Out<int32_t> o(m->ctx, cond_forward, m->n_nodes);
+      CK(cudaMemcpyAsync(o.dev, m->cond_fwd.p, m->n_nodes * sizeof(int), cudaMemcpyDeviceToDevice, s));
+      o.finish();
+    }
+    if (pinned_dofs) {
+      std::vector<uint8_t> f(3 * m->n_nodes);
+      CK(cudaMemcpyAsync(f.data(), m->pinned.p, f.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::vector<int32_t> list;
+      list.reserve(m->n_pins);
+      for (size_t i = 0; i < f.size(); ++i)
+        if (f[i]) list.push_back((int32_t)i);
+      CK(cudaMemcpy(pinned_dofs, list.data(), list.size() * sizeof(int32_t), cudaMemcpyDefault));
+    }
+    if (tets) CK(cudaMemcpy(tets, m->h_tets.data(), m->h_tets.size() * sizeof(int32_t), cudaMemcpyDefault));
+  });
+}
+
+// ---- materials ------------------------------------------------------------
+int ect_harmonic_mu_tilde(ect_mesh* m, const ect_materials* mats, double* out) {
+  return guarded([&] {
+    // harmonic_mu_tilde (materials.cpp:32-42): sequential fold in tet order
+    double vol = 0.0, weighted = 0.0;
+    for (int64_t t = 0; t < m->n_tets; ++t) {
+      const int32_t* k = &m->h_tets[4 * t];
+      const double v = signed_volume_host(&m->h_xyz[3 * k[0]], &m->h_xyz[3 * k[1]],
+                                          &m->h_xyz[3 * k[2]], &m->h_xyz[3 * k[3]]);
+      vol += v;
+      weighted += v / mats->mu[m->h_region[t]];
+    }
+    require(weighted > 0.0, ECT_ERR_CONFIG, "harmonic_mu_tilde: mesh has no volume");
+    *out = vol / weighted;
+  });
+}
+
+int ect_materials_from_physics(ect_mesh* mesh, const ect_physics* ph, ect_materials* primary,
+                               ect_materials* reference, int32_t* two_configs) {
+  return guarded([&] {
+    // RunConfig::material_table (config.cpp:325-347); TSP keeps its defaults
+    // (config.hpp:29-30), IBC off.
+    require(ph->frequency > 0 && ph->sigma_tube >= 0, ECT_ERR_CONFIG, "physics: bad frequency/sigma");
+    ect_materials m{};
+    m.omega = 2.0 * std::numbers::pi * ph->frequency;
+    m.sigma_eps = ph->sigma_eps_ratio * ph->sigma_tube;
+    m.delta_gauge = ph->delta_gauge;
+    m.bc_penalty = ph->bc_penalty;
+    m.l22_use_sigma_eps = 0;
+    m.ibc_enabled = 0;
+    auto set = [&m](int r, double s, double mu) {
+      m.sigma[r] = s;
+      m.mu[r] = mu;
+    };
+    set(ECT_REGION_TUBE, ph->sigma_tube, kMu0 * ph->mu_r_tube);
+    set(ECT_REGION_TSP, 5e6, kMu0 * 50.0);
+    set(ECT_REGION_DEFECT, ph->sigma_defect >= 0 ? ph->sigma_defect : ph->sigma_tube,
+        kMu0 * (ph->mu_r_defect >= 0 ? ph->mu_r_defect : ph->mu_r_tube));
+    set(ECT_REGION_COIL1, 0.0, kMu0);
+    set(ECT_REGION_COIL2, 0.0, kMu0);
+    set(ECT_REGION_VACUUM, 0.0, kMu0);
+    // resolve_mu_tilde (config.cpp:349-352)
+    if (ph->mu_tilde_harmonic) {
+      int rc = ect_harmonic_mu_tilde(mesh, &m, &m.mu_tilde);
+      if (rc) ect::fail(rc, g_last_error);
+    } else {
+      m.mu_tilde = ph->mu_tilde_fixed;
+    }
+    // reference_variant (materials.cpp:44-53)
+    ect_materials r = m;
+    r.sigma[ECT_REGION_DEFECT] = m.sigma_eps;
+    r.mu[ECT_REGION_DEFECT] = kMu0;
+    r.sigma[ECT_REGION_VACUUM] = m.sigma_eps;
+    r.sigma[ECT_REGION_COIL1] = m.sigma_eps;
+    r.sigma[ECT_REGION_COIL2] = m.sigma_eps;
+    if (primary) *primary = m;
+    if (reference) *reference = r;
+    // scan.cpp:46-49
+    if (two_configs) *two_configs = mesh->n_defect > 0 && !same_coefficients(m, r);
+  });
+}
+
+// ---- matrix -----------------------------------------------------------------
+int ect_matrix_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix** out) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    auto a = std::make_unique<ect_matrix>();
+    a->ctx = ctx;
+    EventTimer t(ctx, &ctx->timings.pattern_ms);
+    ect::build_pattern(mesh, a.get());
+    *out = a.release();
+  });
+}
+
+int ect_matrix_from_csr(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* row_ptr,
+                        const int32_t* col_idx, const double* values, ect_matrix** out) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(n > 0 && nnz > 0 && nnz < (1ll << 31), ECT_ERR_SOLVER, "from_csr: bad dimensions");
+    auto a = std::make_unique<ect_matrix>();
+    a->ctx = ctx;
+    a->n = n;
+    a->nnz = nnz;
+    a->row_ptr.alloc(n + 1);
+    a->col.alloc(nnz);
+    a->val.alloc(nnz);
+    CK(cudaMemcpyAsync(a->row_ptr.p, row_ptr, (n + 1) * sizeof(int), cudaMemcpyDefault, ctx->stream));
+    CK(cudaMemcpyAsync(a->col.p, col_idx, nnz * sizeof(int), cudaMemcpyDefault, ctx->stream));
+    CK(cudaMemcpyAsync(a->val.p, values, nnz * sizeof(double2), cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    a->assembled = true;
+    ect::compute_jacobi(a.get());
+    *out = a.release();
+  });
+}
+
+int ect_matrix_destroy(ect_matrix* a) {
+  return guarded([&] {
+    if (!a) return;
+    ScopedDevice sd(a->ctx->device);
+    delete a;
+  });
+}
+
+int ect_matrix_counts(ect_matrix* a, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    if (n) *n = a->n;
+    if (nnz) *nnz = a->nnz;
+  });
+}
+
+int ect_matrix_assemble(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* mats, ect_matrix* a) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    check_materials(*mats);
+    EventTimer t(ctx, &ctx->timings.assemble_ms);
+    ect::assemble_values(mesh, *mats, a);
+  });
+}
+
+int ect_matrix_export(ect_matrix* a, int32_t* row_ptr, int32_t* col_idx, double* values) {
+  return guarded([&] {
+    ect_ctx* ctx = a->ctx;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    if (row_ptr) CK(cudaMemcpyAsync(row_ptr, a->row_ptr.p, (a->n + 1) * sizeof(int), cudaMemcpyDefault, ctx->stream));
+    if (col_idx) CK(cudaMemcpyAsync(col_idx, a->col.p, a->nnz * sizeof(int), cudaMemcpyDefault, ctx->stream));
+    if (values) {
+      require(a->assembled, ECT_ERR_SOLVER, "export: matrix values not assembled");
+      CK(cudaMemcpyAsync(values, a->val.p, a->nnz * sizeof(double2), cudaMemcpyDefault, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---- rhs / spmv / solve ------------------------------------------------------
+int ect_rhs_coil(ect_ctx* ctx, ect_mesh* mesh, const ect_coil* coil, const double* probe_z,
+                 const int32_t* which_coil, int32_t n_rhs, double amplitude, double* rhs) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(n_rhs >= 1, ECT_ERR_CONFIG, "rhs: n_rhs must be >= 1");
+    const size_t N = 3 * mesh->n_nodes + mesh->n_cond;
+    std::vector<double> z(probe_z, probe_z + n_rhs);
+    std::vector<int> w(which_coil, which_coil + n_rhs);
+    Out<double2> o(ctx, reinterpret_cast<double2*>(rhs), N * n_rhs);
+    EventTimer t(ctx, &ctx->timings.rhs_ms);
+    ect::build_rhs(mesh, *coil, z.data(), w.data(), n_rhs, amplitude, o.dev);
+    o.finish();
+  });
+}
+
+int ect_spmv(ect_ctx* ctx, ect_matrix* a, const double* x, double* y, int32_t n_rhs) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(a->assembled, ECT_ERR_SOLVER, "spmv: matrix values not assembled");
+    const size_t cnt = (size_t)a->n * n_rhs;
+    In<double2> xi(ctx, reinterpret_cast<const double2*>(x), cnt);
+    Out<double2> yo(ctx, reinterpret_cast<double2*>(y), cnt);
+    ect::spmv(ctx, a, xi.dev, yo.dev, n_rhs);
+    yo.finish();
+  });
+}
+
+int ect_solve(ect_ctx* ctx, ect_matrix* a, const double* b, double* x, int32_t n_rhs,
+              const ect_iter_options* opts, ect_iter_result* results) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(a->assembled, ECT_ERR_SOLVER, "solve: matrix values not assembled");
+    ect_iter_options o = opts ? *opts : ect_iter_options{1e-8, 500, 80};
+    const size_t cnt = (size_t)a->n * n_rhs;
+    In<double2> bi(ctx, reinterpret_cast<const double2*>(b), cnt);
+    Out<double2> xo(ctx, reinterpret_cast<double2*>(x), cnt);
+    ect::SolveOut so;
+    {
+      EventTimer t(ctx, &ctx->timings.solve_ms);
+      ect::cocg_solve(ctx, a, bi.dev, xo.dev, n_rhs, o, &so);
+    }
+    xo.finish();
+    for (int c = 0; c < n_rhs; ++c) {
+      results[c].iterations = so.iters[c];
+      results[c].residual = so.residual[c];
+      results[c].converged = so.converged[c];
+    }
+  });
+}
+
+int ect_delta_impedance(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* primary,
+                        const ect_materials* reference, const double* x_k1, const double* x_k2,
+                        const double* x_l1, const double* x_l2, double* dz) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    const size_t N = 3 * mesh->n_nodes + mesh->n_cond;
+    In<double2> a(ctx, reinterpret_cast<const double2*>(x_k1), N);
+    In<double2> b(ctx, reinterpret_cast<const double2*>(x_k2), N);
+    In<double2> c(ctx, reinterpret_cast<const double2*>(x_l1), N);
+    In<double2> d(ctx, reinterpret_cast<const double2*>(x_l2), N);
+    double2 out[4];
+    ect::delta_impedance(mesh, *primary, *reference, a.dev, b.dev, c.dev, d.dev, 1, out);
+    for (int q = 0; q < 4; ++q) {
+      dz[2 * q] = out[q].x;
+      dz[2 * q + 1] = out[q].y;
+    }
+  });
+}
+
+}  // extern "C"
+
+// ---- ScanSession --------------------------------------------------------------
+struct ect_session {
+  ect_ctx* ctx = nullptr;
+  ect_mesh* mesh = nullptr;
+  ect_materials primary{}, reference{};
+  bool two_configs = false;
+  ect_coil coil{};
+  double amplitude = 1.0;
+  ect_iter_options opts{};
+  ect_matrix* a_primary = nullptr;
+  ect_matrix* a_reference = nullptr;
+  ~ect_session() {
+    delete a_primary;
+    delete a_reference;
+  }
+};
+
+extern "C" {
+
+int ect_session_create(ect_ctx* ctx, ect_mesh* mesh, const ect_physics* physics,
+                       const ect_coil* coil, double amplitude, const ect_iter_options* opts,
+                       ect_session** out) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    auto s = std::make_unique<ect_session>();
+    s->ctx = ctx;
+    s->mesh = mesh;
+    s->coil = *coil;
+    s->amplitude = amplitude;
+    s->opts = opts ? *opts : ect_iter_options{1e-8, 500, 80};
+    int32_t two = 0;
+    int rc = ect_materials_from_physics(mesh, physics, &s->primary, &s->reference, &two);
+    if (rc) ect::fail(rc, g_last_error);
+    s->two_configs = two != 0;
+    // ScanSession ctor (scan.cpp:27-85): assemble once per configuration.
+    rc = ect_matrix_create(ctx, mesh, &s->a_primary);
+    if (rc) ect::fail(rc, g_last_error);
+    rc = ect_matrix_assemble(ctx, mesh, &s->primary, s->a_primary);
+    if (rc) ect::fail(rc, g_last_error);
+    if (s->two_configs) {
+      rc = ect_matrix_create(ctx, mesh, &s->a_reference);
+      if (rc) ect::fail(rc, g_last_error);
+      rc = ect_matrix_assemble(ctx, mesh, &s->reference, s->a_reference);
+      if (rc) ect::fail(rc, g_last_error);
+    }
+    *out = s.release();
+  });
+}
+
+int ect_session_destroy(ect_session* s) {
+  return guarded([&] {
+    if (!s) return;
+    ScopedDevice sd(s->ctx->device);
+    delete s;
+  });
+}
+
+int ect_session_matrix(ect_session* s, int reference, ect_matrix** out) {
+  return guarded([&] {
+    *out = reference ? s->a_reference : s->a_primary;
+    require(*out != nullptr, ECT_ERR_CONFIG, "session has no reference configuration");
+  });
+}
+
+int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
+                                int32_t positions_per_batch, ect_signal_point* out,
+                                double* solutions) {
+  return guarded([&] {
+    ect_ctx* ctx = s->ctx;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(positions_per_batch >= 1 && positions_per_batch <= 8, ECT_ERR_CONFIG,
+            "positions_per_batch must be in 1..8");
+    const int64_t N = 3 * s->mesh->n_nodes + s->mesh->n_cond;
+    const int P = positions_per_batch;
+    const int kmax = 2 * P;
+    ect::DevBuf<double2> rhs((size_t)N * kmax), xp((size_t)N * kmax), xr((size_t)N * kmax);
+    for (int p0 = 0; p0 < n_pos; p0 += P) {
+      const int np = std::min(P, n_pos - p0);
+      const int k = 2 * np;
+      // solve_position (scan.cpp:95-143): coil 1 and coil 2 right-hand sides
+      std::vector<double> zz(k);
+      std::vector<int> ww(k);
+      for (int q = 0; q < np; ++q) {
+        zz[2 * q] = zz[2 * q + 1] = z[p0 + q];
+        ww[2 * q] = 1;
+        ww[2 * q + 1] = 2;
+      }
+      std::vector<ect_signal_point> pts(np);
+      for (int q = 0; q < np; ++q) {
+        std::memset(&pts[q], 0, sizeof(ect_signal_point));
+        pts[q].z = z[p0 + q];
+      }
+      try {
+        {
+          EventTimer t(ctx, &ctx->timings.rhs_ms);
+          ect::build_rhs(s->mesh, s->coil, zz.data(), ww.data(), k, s->amplitude, rhs.p);
+        }
+        ect::SolveOut sp, sr;
+        {
+          EventTimer t(ctx, &ctx->timings.solve_ms);
+          ect::cocg_solve(ctx, s->a_primary, rhs.p, xp.p, k, s->opts, &sp);
+          if (s->two_configs) ect::cocg_solve(ctx, s->a_reference, rhs.p, xr.p, k, s->opts, &sr);
+        }
+        for (int q = 0; q < np; ++q) {
+          ect_signal_point& pt = pts[q];
+          bool ok = sp.converged[2 * q] && sp.converged[2 * q + 1];
+          pt.iterations[0] = sp.iters[2 * q];
+          pt.iterations[1] = sp.iters[2 * q + 1];
+          if (s->two_configs) {
+            ok = ok && sr.converged[2 * q] && sr.converged[2 * q + 1];
+            pt.iterations[2] = sr.iters[2 * q];
+            pt.iterations[3] = sr.iters[2 * q + 1];
+          }
+          if (!ok) {
+            pt.failed = 1;  // scan.cpp:111-114,139-141
+            continue;
+          }
+          double2 dz[4] = {};
+          if (s->two_configs) {
+            ect::delta_impedance(s->mesh, s->primary, s->reference, xp.p + 2 * q,
+                                 xp.p + 2 * q + 1, xr.p + 2 * q, xr.p + 2 * q + 1, k, dz);
+          }
+          for (int j = 0; j < 4; ++j) {
+            pt.dz[2 * j] = dz[j].x;
+            pt.dz[2 * j + 1] = dz[j].y;
+          }
+          // signal_modes (signals.cpp:101-107): Z_FA = (i/2)(Z11 + Z12), Z_F3 = (i/2)(Z11 - Z22)
+          const double s_re = dz[0].x + dz[1].x, s_im = dz[0].y + dz[1].y;
+          const double d_re = dz[0].x - dz[3].x, d_im = dz[0].y - dz[3].y;
+          pt.z_fa[0] = 0.0 * s_re - 0.5 * s_im;
+          pt.z_fa[1] = 0.0 * s_im + 0.5 * s_re;
+          pt.z_f3[0] = 0.0 * d_re - 0.5 * d_im;
+          pt.z_f3[1] = 0.0 * d_im + 0.5 * d_re;
+        }
+        if (solutions && p0 + np == n_pos) {
+          // 4 solution vectors of the last position: primary c1, c2, reference c1, c2
+          const int q = np - 1;
+          double2* dst = reinterpret_cast<double2*>(solutions);
+          const bool dev = ect::is_device_ptr(solutions);
+          const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+          for (int v = 0; v < 4; ++v) {
+            const double2* src = (v < 2 ? xp.p : xr.p) + 2 * q + (v & 1);
+            if (v >= 2 && !s->two_configs) src = xp.p + 2 * q + (v & 1);
+            CK(cudaMemcpy2DAsync(dst + v * N, sizeof(double2), src, k * sizeof(double2),
+                                 sizeof(double2), N, kind, ctx->stream));
+          }
+          CK(cudaStreamSynchronize(ctx->stream));
+        }
+      } catch (const ect::Error& e) {
+        if (e.code != ECT_ERR_SOLVER) throw;
+        for (auto& pt : pts) pt.failed = 1;  // SolverError marks the points failed
+      }
+      for (int q = 0; q < np; ++q) out[p0 + q] = pts[q];
+    }
+  });
+}
+
+}  // extern "C"

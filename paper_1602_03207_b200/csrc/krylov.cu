@@ -1,0 +1,694 @@
+// K4 SpMV/SpMM + K5 fused Krylov vector ops + K6 device-resident COCG.
+//
+// Replaces CscMatrix::multiply (sparse.cpp:115-124), vector_norm /
+// relative_residual (sparse.cpp:126-145) and solve_iterative
+// (iterative.cpp:109-228). The reference runs restarted GMRES(80) with an
+// ILU(0) right preconditioner, serial; A is complex SYMMETRIC (A = A^T, not
+// Hermitian, when IBC is off — SURVEY §8(a)), so the GPU uses Jacobi-
+// preconditioned COCG (conjugate orthogonal CG, unconjugated bilinear form)
+// whose iteration is one SpMV plus fused vector updates: bandwidth-bound and
+// without GMRES's growing basis. Convergence follows the reference contract:
+// recurrence residual <= tol, then a TRUE residual confirmation
+// (iterative.cpp:208-216) with restart when it fails; b == 0 -> x = 0
+// converged (iterative.cpp:120-124); non-convergence is a flag, breakdown an
+// error (iterative.cpp:176).
+//
+// Layout: CSR values double2 (16 B), int32 columns; vectors for k
+// right-hand sides are interleaved [n][k] double2 so one gather serves all
+// k columns (multi-RHS sweep, SURVEY §8(d) B_iter(k)).
+// Determinism: grid-stride persistent grids with a static row->thread map,
+// fixed-order warp/block trees, and a last-block fixed-order reduction of the
+// per-block partials — bitwise-repeatable, no fp64 atomics.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <thread>
+
+#include "ect_internal.h"
+
+namespace ect {
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+// Smith's complex division a / b
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    double r = b.y / b.x, den = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+  }
+  double r = b.x / b.y, den = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+
+__device__ __forceinline__ double2 ldg2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_i(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Block-wide sum of NV doubles per thread into smem-backed result (thread 0).
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) smem[wid * NV + j] = v[j];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double x = lane < nw ? smem[lane * NV + j] : 0.0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      v[j] = x;
+    }
+  }
+  __syncthreads();
+}
+
+// Last-block-done: returns true in the block that finished last (all of
+// whose threads then see every other block's partials).
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned ticket = atomicAdd(counter, 1u);
+    is_last = ticket == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Fixed-order reduction of NV values per block stored at partial[b*NV + j].
+template <int NV>
+__device__ __forceinline__ void reduce_partials(const double* partial, double (&out)[NV],
+                                                double* smem) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) out[j] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) out[j] += __ldcg(partial + (size_t)b * NV + j);
+  block_sum<NV>(out, smem);
+}
+
+enum Mode { kPlain = 0, kCocg = 1, kResid = 2 };
+
+struct KrylovCtl {
+  RhsState* st;       // [K]
+  int* n_active;
+  unsigned* counter;
+  double* partial;    // [grid][NV]
+  double tol;
+  int max_iter;
+};
+
+// y = A x for K interleaved vectors with G lanes per row.
+//  kPlain: y = A x
+//  kCocg : y = q = A p; per column p^T q (unconjugated) -> alpha = rho / p^T q
+//  kResid: y = b - A x; per column ||y||^2 -> st.rnorm (true residual)
+template <int G, int K, int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
+       const double2* __restrict__ val, const double2* __restrict__ x, double2* __restrict__ y,
+       const double2* __restrict__ b, KrylovCtl ctl) {
+  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
+  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  bool act[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) act[k] = (MODE == kPlain) || ctl.st[k].status == kActive;
+
+  constexpr int RPW = 32 / G;  // rows per warp and pass
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+
+  // warp-uniform trip count so the segment shuffles always see full warps
+  for (int64_t wrow = warp * RPW; wrow < n; wrow += n_warps * RPW) {
+    const int64_t row = wrow + lane / G;
+    const bool valid = row < n;
+    const int beg = valid ? row_ptr[row] : 0, end = valid ? row_ptr[row + 1] : 0;
+    double2 acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+    int p = beg + g;
+    // 2-deep software pipeline on the streamed matrix entries
+    for (; p + G < end; p += 2 * G) {
+      const int j0 = ldg_i(col + p), j1 = ldg_i(col + p + G);
+      const double2 a0 = ldg2(val + p), a1 = ldg2(val + p + G);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        const double2 x0 = x[(int64_t)j0 * K + k], x1 = x[(int64_t)j1 * K + k];
+        acc[k].x += a0.x * x0.x - a0.y * x0.y;
+        acc[k].y += a0.x * x0.y + a0.y * x0.x;
+        acc[k].x += a1.x * x1.x - a1.y * x1.y;
+        acc[k].y += a1.x * x1.y + a1.y * x1.x;
+      }
+    }
+    if (p < end) {
+      const int j0 = ldg_i(col + p);
+      const double2 a0 = ldg2(val + p);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        const double2 x0 = x[(int64_t)j0 * K + k];
+        acc[k].x += a0.x * x0.x - a0.y * x0.y;
+        acc[k].y += a0.x * x0.y + a0.y * x0.x;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int o = G / 2; o; o >>= 1) {
+        acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, o, G);
+        acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, o, G);
+      }
+    }
+    if (g == 0 && valid) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        const int64_t idx = row * K + k;
+        if (MODE == kPlain) {
+          y[idx] = acc[k];
+        } else if (MODE == kCocg) {
+          y[idx] = acc[k];
+          const double2 pv = x[idx];
+          part[2 * k] += pv.x * acc[k].x - pv.y * acc[k].y;
+          part[2 * k + 1] += pv.x * acc[k].y + pv.y * acc[k].x;
+        } else {
+          const double2 rv = csub(b[idx], acc[k]);
+          y[idx] = rv;
+          part[k] += rv.x * rv.x + rv.y * rv.y;
+        }
+      }
+    }
+  }
+  if (MODE == kPlain) return;
+
+  block_sum<NV>(part, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    if (MODE == kCocg) {
+      int active = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        RhsState& s = ctl.st[k];
+        if (s.status != kActive) continue;
+        const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
+        if (pq.x == 0.0 && pq.y == 0.0) {
+          s.status = kBreakdown;
+          continue;
+        }
+        s.alpha = cdiv(s.rho, pq);
+        ++active;
+      }
+      *ctl.n_active = active;
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
+// x += alpha p ; r -= alpha q ; z = D^-1 r ; partial r^T z, ||r||^2
+// last block: convergence test, beta, rho.
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const double2* __restrict__ p,
+         const double2* __restrict__ q, const double2* __restrict__ dinv, KrylovCtl ctl) {
+  constexpr int NV = 3 * K;
+  __shared__ double smem[32 * NV];
+  if (*ctl.n_active == 0) return;
+  bool act[K];
+  double2 alpha[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    act[k] = ctl.st[k].status == kActive;
+    alpha[k] = ctl.st[k].alpha;
+  }
+  double part[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 d = dinv[i];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!act[k]) continue;
+      const int64_t idx = i * K + k;
+      const double2 pv = p[idx], qv = q[idx];
+      double2 xv = x[idx], rv = r[idx];
+      xv = cadd(xv, cmul(alpha[k], pv));
+      rv = csub(rv, cmul(alpha[k], qv));
+      x[idx] = xv;
+      r[idx] = rv;
+      const double2 z = cmul(d, rv);
+      part[3 * k] += rv.x * z.x - rv.y * z.y;
+      part[3 * k + 1] += rv.x * z.y + rv.y * z.x;
+      part[3 * k + 2] += rv.x * rv.x + rv.y * rv.y;
+    }
+  }
+  block_sum<NV>(part, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    int active = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      RhsState& s = ctl.st[k];
+      if (s.status != kActive) continue;
+      const double2 rho_new = make_double2(tot[3 * k], tot[3 * k + 1]);
+      s.rnorm = sqrt(tot[3 * k + 2]);
+      s.iters += 1;
+      if (s.rnorm <= ctl.tol * s.bnorm) {
+        s.status = kConverged;
+      } else if (s.iters >= ctl.max_iter) {
+        s.status = kMaxIter;
+      } else if (rho_new.x == 0.0 && rho_new.y == 0.0) {
+        s.status = kBreakdown;
+      } else {
+        s.beta = cdiv(rho_new, s.rho);
+        s.rho = rho_new;
+        ++active;
+      }
+    }
+    *ctl.n_active = active;
+    *ctl.counter = 0u;
+  }
+}
+
+// p = D^-1 r + beta p
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_pupdate(int64_t n, const double2* __restrict__ r, double2* __restrict__ p,
+          const double2* __restrict__ dinv, KrylovCtl ctl) {
+  if (*ctl.n_active == 0) return;
+  bool act[K];
+  double2 beta[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    act[k] = ctl.st[k].status == kActive;
+    beta[k] = ctl.st[k].beta;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 d = dinv[i];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!act[k]) continue;
+      const int64_t idx = i * K + k;
+      p[idx] = cadd(cmul(d, r[idx]), cmul(beta[k], p[idx]));
+    }
+  }
+}
+
+// (Re)start selected columns from their residual r: p = D^-1 r, rho = r^T z,
+// ||r||; on a fresh start also x = 0, r = b and bnorm = ||b||.
+// mask bit k set -> (re)start column k.
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, double2* __restrict__ r,
+        double2* __restrict__ p, const double2* __restrict__ dinv, unsigned mask, int fresh,
+        KrylovCtl ctl) {
+  constexpr int NV = 4 * K;
+  __shared__ double smem[32 * NV];
+  double part[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 d = dinv[i];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!((mask >> k) & 1u)) continue;
+      const int64_t idx = i * K + k;
+      double2 rv;
+      if (fresh) {
+        rv = b[idx];
+        x[idx] = make_double2(0.0, 0.0);
+        r[idx] = rv;
+        part[4 * k + 3] += rv.x * rv.x + rv.y * rv.y;
+      } else {
+        rv = r[idx];
+      }
+      const double2 z = cmul(d, rv);
+      p[idx] = z;
+      part[4 * k] += rv.x * z.x - rv.y * z.y;
+      part[4 * k + 1] += rv.x * z.y + rv.y * z.x;
+      part[4 * k + 2] += rv.x * rv.x + rv.y * rv.y;
+    }
+  }
+  block_sum<NV>(part, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    int active = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      RhsState& s = ctl.st[k];
+      if ((mask >> k) & 1u) {
+        if (fresh) {
+          s.bnorm = sqrt(tot[4 * k + 3]);
+          s.iters = 0;
+        }
+        s.rho = make_double2(tot[4 * k], tot[4 * k + 1]);
+        s.rnorm = sqrt(tot[4 * k + 2]);
+        if (fresh && s.bnorm == 0.0) {
+          s.status = kZeroRhs;
+        } else if (s.rnorm <= ctl.tol * s.bnorm) {
+          s.status = kConverged;
+        } else if (s.rho.x == 0.0 && s.rho.y == 0.0) {
+          s.status = kBreakdown;
+        } else {
+          s.status = kActive;
+        }
+      }
+      active += s.status == kActive;
+    }
+    *ctl.n_active = active;
+    *ctl.counter = 0u;
+  }
+}
+
+__global__ void k_jacobi(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                         const double2* __restrict__ val, double2* dinv, int* missing) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = row_ptr[i], hi = row_ptr[i + 1] - 1;
+    int pos = -1;
+    while (lo <= hi) {
+      int mid = (lo + hi) >> 1;
+      int c = col[mid];
+      if (c == i) { pos = mid; break; }
+      if (c < i) lo = mid + 1; else hi = mid - 1;
+    }
+    double2 d = pos >= 0 ? val[pos] : make_double2(0.0, 0.0);
+    if (d.x == 0.0 && d.y == 0.0) {
+      atomicAdd(missing, 1);
+      dinv[i] = make_double2(1.0, 0.0);
+    } else {
+      dinv[i] = cdiv(make_double2(1.0, 0.0), d);
+    }
+  }
+}
+
+struct Launch {
+  int grid_spmv = 0, grid_vec = 0;
+};
+
+template <int K>
+struct Dispatch {
+  static void spmv(ect_ctx* ctx, int mode, int grid, int64_t n, const ect_matrix* a,
+                   const double2* x, double2* y, const double2* b, KrylovCtl ctl) {
+    cudaStream_t s = ctx->stream;
+    constexpr int G = K >= 4 ? 8 : 16;
+    if (mode == kPlain)
+      k_spmv<G, K, kPlain><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
+    else if (mode == kCocg)
+      k_spmv<G, K, kCocg><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
+    else
+      k_spmv<G, K, kResid><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
+    CK_LAUNCH();
+  }
+  static void update(ect_ctx* ctx, int grid, int64_t n, double2* x, double2* r, const double2* p,
+                     const double2* q, const double2* dinv, KrylovCtl ctl) {
+    k_update<K><<<grid, kBlock, 0, ctx->stream>>>(n, x, r, p, q, dinv, ctl);
+    CK_LAUNCH();
+  }
+  static void pupdate(ect_ctx* ctx, int grid, int64_t n, const double2* r, double2* p,
+                      const double2* dinv, KrylovCtl ctl) {
+    k_pupdate<K><<<grid, kBlock, 0, ctx->stream>>>(n, r, p, dinv, ctl);
+    CK_LAUNCH();
+  }
+  static void start(ect_ctx* ctx, int grid, int64_t n, const double2* b, double2* x, double2* r,
+                    double2* p, const double2* dinv, unsigned mask, int fresh, KrylovCtl ctl) {
+    k_start<K><<<grid, kBlock, 0, ctx->stream>>>(n, b, x, r, p, dinv, mask, fresh, ctl);
+    CK_LAUNCH();
+  }
+  static int spmv_grid(ect_ctx* ctx, int mode) {
+    constexpr int G = K >= 4 ? 8 : 16;
+    const void* f = mode == kPlain  ? (const void*)k_spmv<G, K, kPlain>
+                    : mode == kCocg ? (const void*)k_spmv<G, K, kCocg>
+                                    : (const void*)k_spmv<G, K, kResid>;
+    return grid_for(ctx, f, kBlock);
+  }
+  static int vec_grid(ect_ctx* ctx) { return grid_for(ctx, (const void*)k_update<K>, kBlock); }
+};
+
+// Runs fn with the Dispatch<K> matching k.
+template <typename F>
+void with_k(int k, F&& fn) {
+  switch (k) {
+    case 1: fn(Dispatch<1>{}); break;
+    case 2: fn(Dispatch<2>{}); break;
+    case 4: fn(Dispatch<4>{}); break;
+    case 8: fn(Dispatch<8>{}); break;
+    case 16: fn(Dispatch<16>{}); break;
+    default: fail(ECT_ERR_SOLVER, "unsupported right-hand-side batch width " + std::to_string(k));
+  }
+}
+
+void prof_begin(ect_ctx* ctx, cudaEvent_t* ev) {
+  if (!ctx->prof.enabled) return;
+  auto& P = ctx->prof;
+  if (P.used + 2 > P.pool.size()) {
+    for (int i = 0; i < 512; ++i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      P.pool.push_back(e);
+    }
+  }
+  ev[0] = P.pool[P.used++];
+  ev[1] = P.pool[P.used++];
+  CK(cudaEventRecord(ev[0], ctx->stream));
+}
+void prof_end(ect_ctx* ctx, cudaEvent_t* ev) {
+  if (!ctx->prof.enabled) return;
+  CK(cudaEventRecord(ev[1], ctx->stream));
+}
+void prof_collect(ect_ctx* ctx) {
+  auto& P = ctx->prof;
+  if (!P.enabled || P.used == 0) return;
+  CK(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < P.used; i += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, P.pool[i], P.pool[i + 1]));
+    tot += ms;
+  }
+  ctx->timings.spmv_ms_total += tot;
+  ctx->timings.spmv_launches += (int64_t)(P.used / 2);
+  P.used = 0;
+}
+
+}  // namespace
+
+void compute_jacobi(ect_matrix* a) {
+  ect_ctx* ctx = a->ctx;
+  a->dinv.alloc(std::max<int64_t>(1, a->n));
+  DevBuf<int> missing(1);
+  CK(cudaMemsetAsync(missing.p, 0, sizeof(int), ctx->stream));
+  int grid = (int)std::min<int64_t>((a->n + 255) / 256, (int64_t)ctx->num_sms * 16);
+  k_jacobi<<<std::max(grid, 1), 256, 0, ctx->stream>>>(a->n, a->row_ptr.p, a->col.p, a->val.p,
+                                                        a->dinv.p, missing.p);
+  CK_LAUNCH();
+  note_launch(ctx, 1);
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, missing.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  (void)h;  // zero diagonals fall back to identity scaling (reported by the solve if singular)
+}
+
+void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
+  with_k(k, [&](auto D) {
+    using DK = decltype(D);
+    KrylovCtl ctl{};
+    const int grid = DK::spmv_grid(ctx, kPlain);
+    cudaEvent_t ev[2];
+    prof_begin(ctx, ev);
+    DK::spmv(ctx, kPlain, grid, a->n, a, x, y, nullptr, ctl);
+    prof_end(ctx, ev);
+    note_launch(ctx, 1);
+  });
+  prof_collect(ctx);
+}
+
+void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
+                const ect_iter_options& opt, SolveOut* out) {
+  if (!(opt.tol > 0.0)) fail(ECT_ERR_SOLVER, "solve_iterative: tolerance must be positive");
+  if (k < 1 || k > 16) fail(ECT_ERR_SOLVER, "solve: n_rhs must be in 1..16");
+  int kk = 1;
+  while (kk < k) kk <<= 1;  // internal batch width (padding columns stay at b = 0)
+  const int64_t n = a->n;
+  cudaStream_t s = ctx->stream;
+
+  out->iters.assign(k, 0);
+  out->residual.assign(k, 0.0);
+  out->converged.assign(k, 0);
+
+  with_k(kk, [&](auto D) {
+    using DK = decltype(D);
+    const int grid_s = DK::spmv_grid(ctx, kCocg);
+    const int grid_r = DK::spmv_grid(ctx, kResid);
+    const int grid_v = DK::vec_grid(ctx);
+    const int grid_max = std::max(std::max(grid_s, grid_r), grid_v);
+    const size_t vec = (size_t)n * kk;
+    DevBuf<double2> bb(vec), xx(vec), r(vec), p(vec), q(vec);
+    DevBuf<RhsState> st(kk);
+    DevBuf<int> n_active(1);
+    DevBuf<unsigned> counter(1);
+    DevBuf<double> partial((size_t)grid_max * 4 * kk);
+    CK(cudaMemsetAsync(st.p, 0, st.bytes(), s));
+    CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(n_active.p, 0, sizeof(int), s));
+    // b in internal layout (zero-padded columns)
+    if (kk == k) {
+      CK(cudaMemcpyAsync(bb.p, b, vec * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    } else {
+      CK(cudaMemsetAsync(bb.p, 0, bb.bytes(), s));
+      CK(cudaMemcpy2DAsync(bb.p, kk * sizeof(double2), b, k * sizeof(double2),
+                           k * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+    }
+    KrylovCtl ctl{st.p, n_active.p, counter.p, partial.p, opt.tol, opt.max_iter};
+    const unsigned all = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
+    DK::start(ctx, grid_v, n, bb.p, xx.p, r.p, p.p, a->dinv.p, all, 1, ctl);
+    note_launch(ctx, 1);
+
+    std::vector<RhsState> hs(kk);
+    int* flag = ctx->pinned_flag;
+    const int chunk = 32;
+    for (int restart_round = 0;; ++restart_round) {
+      // ---- iterate until no column is active ------------------------------
+      int polls_in_flight = 0;
+      cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
+      int launched = 0;
+      const int cap = opt.max_iter + chunk;  // iterations can never exceed max_iter
+      for (; opt.max_iter > 0;) {
+        for (int it = 0; it < chunk; ++it) {
+          cudaEvent_t ev[2];
+          prof_begin(ctx, ev);
+          DK::spmv(ctx, kCocg, grid_s, n, a, p.p, q.p, nullptr, ctl);
+          prof_end(ctx, ev);
+          DK::update(ctx, grid_v, n, xx.p, r.p, p.p, q.p, a->dinv.p, ctl);
+          DK::pupdate(ctx, grid_v, n, r.p, p.p, a->dinv.p, ctl);
+          note_launch(ctx, 3);
+        }
+        launched += chunk;
+        CK(cudaMemcpyAsync(flag + (polls_in_flight & 1), n_active.p, sizeof(int),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(poll_ev[polls_in_flight & 1], s));
+        ++polls_in_flight;
+        if (polls_in_flight >= 2) {
+          // wait for the previous poll while the current chunk runs
+          const int prev = (polls_in_flight - 2) & 1;
+          CK(cudaEventSynchronize(poll_ev[prev]));
+          if (flag[prev] == 0) break;
+        }
+        if (launched > cap + 2 * chunk) break;
+      }
+      CK(cudaStreamSynchronize(s));
+      prof_collect(ctx);
+      // ---- true residual confirmation (iterative.cpp:208-216) ------------
+      // q <- b - A x (q is free here), st.rnorm <- ||b - A x||
+      CK(cudaMemsetAsync(n_active.p, 0xff, sizeof(int), s));  // force the kernel to run
+      {
+        // mark every column for the residual pass
+        CK(cudaMemcpyAsync(hs.data(), st.p, kk * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<RhsState> tmp = hs;
+        for (auto& t : tmp) t.status = kActive;
+        CK(cudaMemcpyAsync(st.p, tmp.data(), kk * sizeof(RhsState), cudaMemcpyHostToDevice, s));
+        DK::spmv(ctx, kResid, grid_r, n, a, xx.p, q.p, bb.p, ctl);
+        note_launch(ctx, 1);
+        std::vector<RhsState> res(kk);
+        CK(cudaMemcpyAsync(res.data(), st.p, kk * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int c = 0; c < kk; ++c) hs[c].rnorm = res[c].rnorm;  // true ||b - A x||
+        CK(cudaMemcpyAsync(st.p, hs.data(), kk * sizeof(RhsState), cudaMemcpyHostToDevice, s));
+      }
+      unsigned restart_mask = 0;
+      for (int c = 0; c < k; ++c) {
+        RhsState& t = hs[c];
+        if (t.status == kBreakdown) {
+          fail(ECT_ERR_SOLVER, "COCG breakdown (p^T A p or r^T z vanished) on right-hand side " +
+                                   std::to_string(c));
+        }
+        const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
+        if (t.status == kConverged && rel > opt.tol && t.iters < opt.max_iter &&
+            restart_round < 8) {
+          restart_mask |= 1u << c;
+        }
+      }
+      if (!restart_mask) break;
+      // restart failed columns from their true residual: r <- b - A x
+      for (int c = 0; c < kk; ++c)
+        if ((restart_mask >> c) & 1u)
+          CK(cudaMemcpy2DAsync(r.p + c, kk * sizeof(double2), q.p + c, kk * sizeof(double2),
+                               sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+      DK::start(ctx, grid_v, n, bb.p, xx.p, r.p, p.p, a->dinv.p, restart_mask, 0, ctl);
+      note_launch(ctx, 1);
+      // keep the other columns frozen
+      CK(cudaStreamSynchronize(s));
+    }
+    for (int c = 0; c < k; ++c) {
+      const RhsState& t = hs[c];
+      out->iters[c] = t.iters;
+      const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
+      out->residual[c] = rel;
+      out->converged[c] = (t.status == kZeroRhs) || (t.status == kConverged && rel <= opt.tol);
+    }
+    if (kk == k) {
+      CK(cudaMemcpyAsync(x, xx.p, vec * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    } else {
+      CK(cudaMemcpy2DAsync(x, k * sizeof(double2), xx.p, kk * sizeof(double2),
+                           k * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+}  // namespace ect

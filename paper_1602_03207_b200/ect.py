@@ -1,0 +1,305 @@
+"""ctypes binding of the ectgpu C ABI (include/ectgpu.h).
+
+This is the Python face of the drop-in boundary: the same entry points a
+cgo/JNI/C++ caller would bind. It mirrors the reference's API names
+(assemble_system/build_global -> Matrix, solve_iterative -> Matrix.solve,
+ScanSession -> Session) and raises the reference's exception classes for the
+ABI status codes (types.hpp:53-64). There is no CPU fallback: importing this
+module on a host without the built library, or creating a Context without a
+B200, fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libectgpu.so"
+
+D, I32, I64, U8 = C.c_double, C.c_int32, C.c_int64, C.c_uint8
+VP = C.c_void_p
+
+
+class EctError(RuntimeError):
+    code = 1
+
+
+class ConfigError(EctError):
+    code = 2
+
+
+class MeshError(EctError):
+    code = 3
+
+
+class SolverError(EctError):
+    code = 4
+
+
+class IoError(EctError):
+    code = 5
+
+
+class CudaError(EctError):
+    code = 6
+
+
+_ERRORS = {2: ConfigError, 3: MeshError, 4: SolverError, 5: IoError, 6: CudaError}
+
+
+class Materials(C.Structure):
+    """ect_materials == MaterialTable (materials.hpp:21-48)."""
+    _fields_ = [("omega", D), ("sigma", D * 6), ("mu", D * 6), ("mu_tilde", D),
+                ("delta_gauge", D), ("bc_penalty", D), ("sigma_eps", D),
+                ("ibc_enabled", I32), ("l22_use_sigma_eps", I32)]
+
+
+class Physics(C.Structure):
+    _fields_ = [("frequency", D), ("sigma_tube", D), ("mu_r_tube", D), ("sigma_defect", D),
+                ("mu_r_defect", D), ("sigma_eps_ratio", D), ("delta_gauge", D),
+                ("bc_penalty", D), ("mu_tilde_harmonic", I32), ("mu_tilde_fixed", D)]
+
+
+class Coil(C.Structure):
+    _fields_ = [("r_inner", D), ("r_outer", D), ("height", D), ("gap", D)]
+
+
+class IterOptions(C.Structure):
+    _fields_ = [("tol", D), ("max_iter", I32), ("restart", I32)]
+
+
+class IterResult(C.Structure):
+    _fields_ = [("residual", D), ("iterations", I32), ("converged", I32)]
+
+
+class SignalPoint(C.Structure):
+    _fields_ = [("z", D), ("dz", D * 8), ("z_fa", D * 2), ("z_f3", D * 2), ("failed", I32),
+                ("iterations", I32 * 4)]
+
+
+class Timings(C.Structure):
+    _fields_ = [("pattern_ms", D), ("assemble_ms", D), ("rhs_ms", D), ("solve_ms", D),
+                ("spmv_ms_total", D), ("spmv_launches", I64), ("kernel_launches", I64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"ectgpu library not built: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(str(LIB_PATH))
+        L.ect_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().ect_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, EctError)(msg)
+
+
+def _ptr(a):
+    """Pointer of a numpy array (host) or a torch tensor (host or device)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def physics_struct(ph) -> Physics:
+    return Physics(ph.frequency, ph.sigma_tube, ph.mu_r_tube, ph.sigma_defect, ph.mu_r_defect,
+                   ph.sigma_eps_ratio, ph.delta_gauge, ph.bc_penalty, int(ph.mu_tilde_harmonic),
+                   ph.mu_tilde_fixed)
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        h = VP()
+        _check(lib().ect_ctx_create(C.c_int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ect_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def timings(self, reset=False) -> dict:
+        t = Timings()
+        _check(lib().ect_ctx_timings(self.h, C.byref(t), C.c_int(int(reset))))
+        return {f: getattr(t, f) for f, _ in Timings._fields_}
+
+    def set_profiling(self, on: bool):
+        _check(lib().ect_ctx_set_profiling(self.h, C.c_int(int(on))))
+
+    def synchronize(self):
+        _check(lib().ect_ctx_synchronize(self.h))
+
+
+class Mesh:
+    """Mesh + ConductorIndexMap + boundary pins, resident on the device."""
+
+    def __init__(self, ctx: Context, xyz, tets, region):
+        self.ctx = ctx
+        xyz = np.ascontiguousarray(xyz, np.float64)
+        tets = np.ascontiguousarray(tets, np.int32)
+        region = np.ascontiguousarray(region, np.uint8)
+        h = VP()
+        _check(lib().ect_mesh_create(ctx.h, _ptr(xyz), I64(xyz.shape[0]), _ptr(tets),
+                                     _ptr(region), I64(tets.shape[0]), C.byref(h)))
+        self.h = h
+        c = (I64 * 6)()
+        _check(lib().ect_mesh_counts(h, c))
+        (self.n_nodes, self.n_tets, self.n_cond, self.n_dofs, self.n_pins,
+         self.n_defect) = list(c)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ect_mesh_destroy(self.h)
+            self.h = None
+
+    def export(self):
+        fwd = np.empty(self.n_nodes, np.int32)
+        pins = np.empty(self.n_pins, np.int32)
+        tets = np.empty((self.n_tets, 4), np.int32)
+        _check(lib().ect_mesh_export(self.h, _ptr(fwd), _ptr(pins), _ptr(tets)))
+        return {"cond_forward": fwd, "pinned_dofs": pins, "tets": tets}
+
+    def materials(self, physics):
+        p, r, two = Materials(), Materials(), I32()
+        ph = physics_struct(physics)
+        _check(lib().ect_materials_from_physics(self.h, C.byref(ph), C.byref(p), C.byref(r),
+                                                C.byref(two)))
+        return p, r, bool(two.value)
+
+    def rhs(self, coil, z, which, amplitude, out=None):
+        z = np.ascontiguousarray(np.atleast_1d(z), np.float64)
+        which = np.ascontiguousarray(np.atleast_1d(which), np.int32)
+        k = z.shape[0]
+        if out is None:
+            out = np.empty((self.n_dofs, k), np.complex128)
+        cs = Coil(*coil)
+        _check(lib().ect_rhs_coil(self.ctx.h, self.h, C.byref(cs), _ptr(z), _ptr(which), I32(k),
+                                  D(amplitude), _ptr(out)))
+        return out
+
+    def delta_impedance(self, primary, reference, xk1, xk2, xl1, xl2):
+        arrs = [np.ascontiguousarray(v, np.complex128) if not hasattr(v, "data_ptr") else v
+                for v in (xk1, xk2, xl1, xl2)]
+        dz = np.empty(8)
+        _check(lib().ect_delta_impedance(self.ctx.h, self.h, C.byref(primary), C.byref(reference),
+                                         *[_ptr(a) for a in arrs], _ptr(dz)))
+        return dz.view(np.complex128)
+
+
+class Matrix:
+    """Global CSR system (pattern bit-identical to the reference CSC)."""
+
+    def __init__(self, ctx: Context, mesh: Mesh | None = None, *, csr=None):
+        self.ctx = ctx
+        h = VP()
+        if csr is not None:
+            row_ptr, col, val = (np.ascontiguousarray(csr[0], np.int32),
+                                 np.ascontiguousarray(csr[1], np.int32),
+                                 np.ascontiguousarray(csr[2], np.complex128))
+            _check(lib().ect_matrix_from_csr(ctx.h, I64(row_ptr.shape[0] - 1), I64(col.shape[0]),
+                                             _ptr(row_ptr), _ptr(col), _ptr(val), C.byref(h)))
+        else:
+            _check(lib().ect_matrix_create(ctx.h, mesh.h, C.byref(h)))
+        self.h = h
+        self.mesh = mesh
+        n, nnz = I64(), I64()
+        _check(lib().ect_matrix_counts(h, C.byref(n), C.byref(nnz)))
+        self.n, self.nnz = n.value, nnz.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and not getattr(self, "_borrowed", False):
+            lib().ect_matrix_destroy(self.h)
+            self.h = None
+
+    def assemble(self, mats: Materials):
+        _check(lib().ect_matrix_assemble(self.ctx.h, self.mesh.h, C.byref(mats), self.h))
+        return self
+
+    def export(self, values=True):
+        rp = np.empty(self.n + 1, np.int32)
+        ci = np.empty(self.nnz, np.int32)
+        v = np.empty(self.nnz, np.complex128) if values else None
+        _check(lib().ect_matrix_export(self.h, _ptr(rp), _ptr(ci), _ptr(v)))
+        return rp, ci, v
+
+    def multiply(self, x, out=None):
+        """y = A x (CscMatrix::multiply); x is [n] or [n, k] interleaved."""
+        k = 1 if x.ndim == 1 else x.shape[1]
+        if out is None:
+            out = np.empty_like(x) if not hasattr(x, "data_ptr") else x.new_empty(x.shape)
+        xs = x if hasattr(x, "data_ptr") else np.ascontiguousarray(x, np.complex128)
+        _check(lib().ect_spmv(self.ctx.h, self.h, _ptr(xs), _ptr(out), I32(k)))
+        return out
+
+    def solve(self, b, tol=1e-8, max_iter=500, restart=80, out=None):
+        """solve_iterative replacement: returns (x, [IterResult dicts])."""
+        k = 1 if b.ndim == 1 else b.shape[1]
+        bs = b if hasattr(b, "data_ptr") else np.ascontiguousarray(b, np.complex128)
+        if out is None:
+            out = np.empty_like(bs) if not hasattr(b, "data_ptr") else b.new_empty(b.shape)
+        opts = IterOptions(tol, max_iter, restart)
+        res = (IterResult * k)()
+        _check(lib().ect_solve(self.ctx.h, self.h, _ptr(bs), _ptr(out), I32(k), C.byref(opts), res))
+        return out, [{"iterations": r.iterations, "residual": r.residual,
+                      "converged": bool(r.converged)} for r in res]
+
+
+class Session:
+    """ScanSession (scan.hpp:39-72) on the GPU."""
+
+    def __init__(self, ctx: Context, mesh: Mesh, physics, coil, amplitude, tol=1e-8,
+                 max_iter=20000, restart=80):
+        self.ctx, self.mesh = ctx, mesh
+        h = VP()
+        ph = physics_struct(physics)
+        cs = Coil(*coil)
+        opts = IterOptions(tol, max_iter, restart)
+        _check(lib().ect_session_create(ctx.h, mesh.h, C.byref(ph), C.byref(cs), D(amplitude),
+                                        C.byref(opts), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ect_session_destroy(self.h)
+            self.h = None
+
+    def matrix(self, reference=False) -> Matrix:
+        h = VP()
+        _check(lib().ect_session_matrix(self.h, C.c_int(int(reference)), C.byref(h)))
+        m = Matrix.__new__(Matrix)
+        m.ctx, m.h, m.mesh, m._borrowed = self.ctx, h, self.mesh, True
+        n, nnz = I64(), I64()
+        _check(lib().ect_matrix_counts(h, C.byref(n), C.byref(nnz)))
+        m.n, m.nnz = n.value, nnz.value
+        return m
+
+    def solve_positions(self, z, positions_per_batch=1, solutions=None):
+        z = np.ascontiguousarray(np.atleast_1d(z), np.float64)
+        pts = (SignalPoint * z.shape[0])()
+        _check(lib().ect_session_solve_positions(self.h, _ptr(z), I32(z.shape[0]),
+                                                 I32(positions_per_batch), pts, _ptr(solutions)))
+        out = []
+        for p in pts:
+            dz = np.array(p.dz[:]).view(np.complex128)
+            out.append({"z": p.z, "dz": dz, "z_fa": complex(p.z_fa[0], p.z_fa[1]),
+                        "z_f3": complex(p.z_f3[0], p.z_f3[1]), "failed": bool(p.failed),
+                        "iterations": list(p.iterations)})
+        return out

@@ -1,0 +1,68 @@
+"""Parity metrics shared by the tests. Test infrastructure."""
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.sparse.csgraph import connected_components
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+SMALL = ["small_4x4x8", "small_6x6x12", "small_5x5x10_nodefect"]
+TUBE, TSP, DEFECT = 0, 1, 2
+
+
+def golden(name):
+    return dict(np.load(GOLDEN / f"{name}.npz"))
+
+
+def value_metrics(vals_a, vals_b, row_ptr, col, pins, penalty):
+    """D10: max |da_ij| / sqrt(|a_ii||a_jj|) and Frobenius relative, both over
+    non-pinned entries; pinned diagonals must equal the penalty exactly."""
+    n = len(row_ptr) - 1
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    diag_pos = np.flatnonzero(rows == col)
+    diag = np.zeros(n, np.complex128)
+    diag[rows[diag_pos]] = vals_b[diag_pos]
+    pinned = np.zeros(n, bool)
+    pinned[pins] = True
+    keep = ~((rows == col) & pinned[rows])
+    d = np.abs(vals_a - vals_b)[keep]
+    scale = np.sqrt(np.abs(diag[rows[keep]]) * np.abs(diag[col[keep]]))
+    max_scaled = float(np.max(d / scale)) if d.size else 0.0
+    frob = float(np.linalg.norm(d) / np.linalg.norm(vals_b[keep]))
+    pin_ok = bool(np.all(vals_a[(rows == col) & pinned[rows]] == penalty))
+    return max_scaled, frob, pin_ok
+
+
+def conductor_components(tets, region, cond_forward):
+    cond = (region == TUBE) | (region == TSP) | (region == DEFECT)
+    t = tets[cond]
+    nc = int(cond_forward.max()) + 1
+    pairs = [(cond_forward[t[:, a]], cond_forward[t[:, b]]) for a in range(4) for b in range(4) if a != b]
+    r = np.concatenate([p[0] for p in pairs])
+    c = np.concatenate([p[1] for p in pairs])
+    g = sp.coo_matrix((np.ones_like(r), (r, c)), shape=(nc, nc))
+    return connected_components(g, directed=False)[1]
+
+
+def solution_errors(x, x_ref, n_nodes, comp):
+    """D9: relative L2 of the A part and of the per-component mean-free V part."""
+    na = 3 * n_nodes
+    ea = np.linalg.norm(x[:na] - x_ref[:na]) / np.linalg.norm(x_ref[:na])
+
+    def mean_free(v):
+        out = v.copy()
+        for c in np.unique(comp):
+            m = comp == c
+            out[m] -= v[m].mean()
+        return out
+
+    va, vb = mean_free(x[na:]), mean_free(x_ref[na:])
+    ev = np.linalg.norm(va - vb) / np.linalg.norm(vb)
+    return float(ea), float(ev)
+
+
+def csr(row_ptr, col, vals):
+    n = len(row_ptr) - 1
+    return sp.csr_matrix((vals, col, row_ptr), shape=(n, n))

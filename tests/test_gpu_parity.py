@@ -1,0 +1,170 @@
+"""GPU parity tests: the sm_100a path through the C ABI vs the reference oracle.
+
+Oracle = the UNMODIFIED ectsim core (oracle/_ref, via the committed golden
+fixtures made by oracle/make_golden.py). Bars:
+  pattern / DOF numbering / pins : bit-exact
+  values                         : bit-exact (GPU restates the reference's IEEE
+                                   sequence); D10 metrics <= 1e-12 asserted too
+  rhs                            : <= 1e-14 relative (hypot may differ by 1 ulp)
+  solution                       : D9 A-part and mean-free V-part rel. L2 <= 1e-6
+  impedance                      : |dZ - dZ*| / max|dZ*| <= 1e-6
+"""
+import numpy as np
+import pytest
+
+from paper_1602_03207_b200 import ect, workloads
+from tests.helpers import (SMALL, conductor_components, csr, golden, solution_errors,
+                           value_metrics)
+
+pytestmark = pytest.mark.gpu
+
+SOLVE_TOL = 1e-10
+
+
+def _mesh(ctx, g):
+    return ect.Mesh(ctx, g["xyz"], g["tets"], g["region"])
+
+
+def _mats(mesh, g, key):
+    p, r, two = mesh.materials(_physics(g))
+    return p if key == "primary" else r
+
+
+def _physics(g):
+    has_defect = bool((g["region"] == 2).any())
+    return workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0) if has_defect else workloads.Physics()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_mesh_prep_matches_reference(ctx, name):
+    g = golden(name)
+    m = _mesh(ctx, g)
+    ex = m.export()
+    assert np.array_equal(ex["cond_forward"], g["cond_forward"])          # conductor_map
+    assert np.array_equal(ex["pinned_dofs"], g["pins"])                   # apply_essential_bc
+    assert np.array_equal(ex["tets"], g["tets"])                          # canonical orientation
+    p, r, two = m.materials(_physics(g))
+    assert two == bool(g["two_configs"])
+    assert p.mu_tilde == g["mats_primary"][13]                            # harmonic mu_tilde, exact
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_pattern_and_values_bit_exact(ctx, name):
+    g = golden(name)
+    m = _mesh(ctx, g)
+    keys = ["primary"] + (["reference"] if bool(g["two_configs"]) else [])
+    p, r, _ = m.materials(_physics(g))
+    for key, mats in zip(keys, (p, r)):
+        a = ect.Matrix(ctx, m).assemble(mats)
+        rp, ci, v = a.export()
+        assert np.array_equal(rp, g[f"{key}_col_ptr"]), "row_ptr != reference col_ptr"
+        assert np.array_equal(ci, g[f"{key}_row_idx"]), "col_idx != reference row_idx"
+        ref_v = g[f"{key}_values"]
+        ms, fr, pin_ok = value_metrics(v, ref_v, rp, ci, g["pins"], mats.bc_penalty)
+        assert pin_ok
+        assert ms <= 1e-12 and fr <= 1e-12, (ms, fr)
+        n_diff = int(np.count_nonzero(v.view(np.uint64) != ref_v.view(np.uint64)))
+        assert n_diff == 0, f"{n_diff} of {v.size * 2} doubles differ bitwise (max scaled {ms:.2e})"
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_rhs_matches_reference(ctx, name):
+    g = golden(name)
+    m = _mesh(ctx, g)
+    z = float(g["z"])
+    b = m.rhs(tuple(g["coil"]), [z, z], [1, 2], float(g["amplitude"]))
+    for c in range(2):
+        ref_b = g["rhs"][c]
+        err = np.linalg.norm(b[:, c] - ref_b) / np.linalg.norm(ref_b)
+        assert err <= 1e-14, err
+        assert np.all(b[3 * m.n_nodes:, c] == 0)                      # scalar tail zero
+        assert np.all(b[g["pins"], c] == 0)                            # pinned entries
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_spmv_matches_reference_multiply(ctx, name):
+    g = golden(name)
+    A = csr(g["primary_col_ptr"], g["primary_row_idx"], g["primary_values"])
+    rng = np.random.default_rng(2)
+    for k in (1, 2, 4, 8):
+        x = rng.uniform(-1, 1, (A.shape[0], k)) + 1j * rng.uniform(-1, 1, (A.shape[0], k))
+        x = np.ascontiguousarray(x if k > 1 else x[:, 0])
+        gm = ect.Matrix(ctx, csr=(g["primary_col_ptr"], g["primary_row_idx"], g["primary_values"]))
+        y = gm.multiply(x)
+        y_ref = A @ x
+        absA = csr(g["primary_col_ptr"], g["primary_row_idx"], np.abs(g["primary_values"]))
+        scale = absA @ np.abs(x)
+        assert np.max(np.abs(y - y_ref) / scale) <= 1e-14
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_solve_matches_direct_reference(ctx, name):
+    g = golden(name)
+    m = _mesh(ctx, g)
+    comp = conductor_components(g["tets"], g["region"], g["cond_forward"])
+    p, r, two = m.materials(_physics(g))
+    for key, mats in zip(["primary"] + (["reference"] if two else []), (p, r)):
+        a = ect.Matrix(ctx, m).assemble(mats)
+        b = np.ascontiguousarray(g["rhs"].T)
+        x, res = a.solve(b, tol=SOLVE_TOL, max_iter=20000)
+        for c in range(2):
+            assert res[c]["converged"], res[c]
+            assert res[c]["residual"] <= SOLVE_TOL
+            ea, ev = solution_errors(x[:, c], g[f"{key}_x"][c], m.n_nodes, comp)
+            assert ea <= 1e-6 and ev <= 1e-6, (key, c, ea, ev)
+            # true residual recomputed on the host from the reference matrix
+            A = csr(g[f"{key}_col_ptr"], g[f"{key}_row_idx"], g[f"{key}_values"])
+            rr = np.linalg.norm(g["rhs"][c] - A @ x[:, c]) / np.linalg.norm(g["rhs"][c])
+            assert rr <= 2 * SOLVE_TOL, rr
+
+
+@pytest.mark.parametrize("name", ["small_4x4x8", "small_6x6x12"])
+def test_delta_impedance_and_session(ctx, name):
+    g = golden(name)
+    m = _mesh(ctx, g)
+    p, r, two = m.materials(_physics(g))
+    assert two
+    xs = [g["primary_x"][0], g["primary_x"][1], g["reference_x"][0], g["reference_x"][1]]
+    dz = m.delta_impedance(p, r, *xs)
+    scale = np.max(np.abs(g["dz"]))
+    assert np.max(np.abs(dz - g["dz"])) / scale <= 1e-12
+    # full ScanSession path: assemble x2, rhs x2, batched COCG, dZ, modes
+    s = ect.Session(ctx, m, _physics(g), tuple(g["coil"]), float(g["amplitude"]), tol=1e-11,
+                    max_iter=20000)
+    pt = s.solve_positions([float(g["z"])])[0]
+    assert not pt["failed"]
+    assert np.max(np.abs(pt["dz"] - g["dz"])) / scale <= 1e-6
+    zfa, zf3 = g["modes"]
+    assert abs(pt["z_fa"] - zfa) / max(abs(zfa), 1e-300) <= 1e-6
+    assert abs(pt["z_f3"] - zf3) / max(abs(zf3), abs(zfa)) <= 1e-6
+
+
+def test_solver_contracts(ctx):
+    """iterative.cpp contracts: b = 0 -> x = 0 converged; tol <= 0 rejected;
+    max_iter = 1 reports non-convergence; bitwise-repeatable solves."""
+    g = golden("small_4x4x8")
+    a = ect.Matrix(ctx, csr=(g["primary_col_ptr"], g["primary_row_idx"], g["primary_values"]))
+    x, res = a.solve(np.zeros(a.n, np.complex128))
+    assert res[0]["converged"] and res[0]["iterations"] == 0 and np.all(x == 0)
+    with pytest.raises(ect.SolverError):
+        a.solve(g["rhs"][0], tol=0.0)
+    x1, r1 = a.solve(g["rhs"][0], tol=1e-14, max_iter=1)
+    assert not r1[0]["converged"] and r1[0]["residual"] > 1e-14
+    xa, _ = a.solve(g["rhs"][0], tol=1e-10, max_iter=5000)
+    xb, _ = a.solve(g["rhs"][0], tol=1e-10, max_iter=5000)
+    assert xa.tobytes() == xb.tobytes()
+
+
+def test_error_paths(ctx):
+    g = golden("small_4x4x8")
+    m = _mesh(ctx, g)
+    with pytest.raises(ect.MeshError):  # empty coil support
+        m.rhs((10.0, 11.0, 1e-3, 0.0), [float(g["z"])], [1], 1.0)
+    with pytest.raises(ect.MeshError):  # support reaching into the conductor slab
+        m.rhs((0.0, 1.0, 1.0, 0.0), [float(g["z"])], [1], 1.0)
+    tets = g["tets"].copy()
+    tets[0, 3] = tets[0, 2]  # degenerate tet
+    with pytest.raises(ect.MeshError):
+        ect.Mesh(ctx, g["xyz"], tets, g["region"])
+    with pytest.raises(ect.MeshError):  # all vacuum: no conductor dofs
+        ect.Mesh(ctx, g["xyz"], g["tets"], np.full_like(g["region"], 5))
