@@ -130,6 +130,10 @@ int ect_ctx_timings(ect_ctx* ctx, ect_timings* out, int reset);
  * iteration; used by bench.py for the roofline figure). */
 int ect_ctx_set_profiling(ect_ctx* ctx, int enabled);
 int ect_ctx_synchronize(ect_ctx* ctx);
+/* Device-side timing on the context stream: record event `slot` (0..7), and
+ * the elapsed ms between two recorded slots (waits for the later one). */
+int ect_ctx_mark(ect_ctx* ctx, int slot);
+int ect_ctx_elapsed_ms(ect_ctx* ctx, int a, int b, double* ms);
 
 /* ---- mesh --------------------------------------------------------------
  * Replaces Mesh construction + canonicalize_orientation (mesh.cpp:50-61),
@@ -170,6 +174,12 @@ int ect_matrix_counts(ect_matrix* m, int64_t* n, int64_t* nnz);
  * (assembly.cpp:74-276, 285-327, 386-419). Deterministic, no fp64 atomics. */
 int ect_matrix_assemble(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* mats, ect_matrix* m);
 int ect_matrix_export(ect_matrix* m, int32_t* row_ptr, int32_t* col_idx, double* values);
+/* The reference's own storage: CscMatrix {col_ptr, row_idx, values}
+ * (sparse.hpp:55-66) of build_global. Pattern arrays equal the CSR ones;
+ * values are A(row_idx[p], col) in column order — bit-identical to the
+ * reference's (A is symmetric only up to rounding, so the CSR and CSC value
+ * arrays are different permutations). */
+int ect_matrix_export_csc(ect_matrix* m, int32_t* col_ptr, int32_t* row_idx, double* values);
 
 /* ---- right-hand sides ----------------------------------------------------
  * K3: coil_support + assemble_rhs + apply_pins_to_rhs for n_rhs (probe z,

@@ -97,7 +97,8 @@ struct ect_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   int* pinned_flag = nullptr;  // small pinned word for convergence polling
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
+  cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
 };
 
 struct ect_mesh {
@@ -144,6 +145,7 @@ bool is_device_ptr(const void* p);
 // Kernel entry points implemented in the .cu files.
 void build_mesh_topology(ect_mesh* m);                         // mesh.cu
 void build_pattern(ect_mesh* m, ect_matrix* a);                // pattern.cu
+void export_csc_values(ect_matrix* a, double2* out);           // pattern.cu (symmetric pattern)
 void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a);  // assembly.cu
 void compute_jacobi(ect_matrix* a);                            // krylov.cu
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k);  // spmv.cu

@@ -91,15 +91,23 @@ struct ScopedDevice {
   }
 };
 
+// Device-time accounting of one phase with its own event pair.
 struct EventTimer {
   ect_ctx* ctx;
   double* slot;
-  EventTimer(ect_ctx* c, double* s) : ctx(c), slot(s) { CK(cudaEventRecord(ctx->ev_a, ctx->stream)); }
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventTimer(ect_ctx* c, double* s) : ctx(c), slot(s) {
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, ctx->stream));
+  }
   ~EventTimer() {
-    if (cudaEventRecord(ctx->ev_b, ctx->stream) != cudaSuccess) return;
-    if (cudaEventSynchronize(ctx->ev_b) != cudaSuccess) return;
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b) == cudaSuccess) *slot += ms;
+    if (cudaEventRecord(b, ctx->stream) == cudaSuccess && cudaEventSynchronize(b) == cudaSuccess) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) *slot += ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
   }
 };
 
@@ -186,6 +194,7 @@ int ect_ctx_create(int device, ect_ctx** out) {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev_a));
     CK(cudaEventCreate(&ctx->ev_b));
+    for (auto& e : ctx->marks) CK(cudaEventCreate(&e));
     CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pinned_flag), 64, cudaHostAllocDefault));
     *out = ctx.release();
   });
@@ -200,6 +209,7 @@ int ect_ctx_destroy(ect_ctx* ctx) {
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
+    for (auto e : ctx->marks) cudaEventDestroy(e);
     ctx->cub_tmp.release();
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -218,6 +228,25 @@ int ect_ctx_set_profiling(ect_ctx* ctx, int enabled) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ctx->prof.enabled = enabled != 0;
+  });
+}
+
+int ect_ctx_mark(ect_ctx* ctx, int slot) {
+  return guarded([&] {
+    require(slot >= 0 && slot < 8, ECT_ERR_OTHER, "ect_ctx_mark: slot must be in 0..7");
+    ScopedDevice sd(ctx->device);
+    CK(cudaEventRecord(ctx->marks[slot], ctx->stream));
+  });
+}
+
+int ect_ctx_elapsed_ms(ect_ctx* ctx, int a, int b, double* ms) {
+  return guarded([&] {
+    require(a >= 0 && a < 8 && b >= 0 && b < 8, ECT_ERR_OTHER, "ect_ctx_elapsed_ms: bad slot");
+    ScopedDevice sd(ctx->device);
+    CK(cudaEventSynchronize(ctx->marks[b]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, ctx->marks[a], ctx->marks[b]));
+    *ms = f;
   });
 }
 
@@ -463,6 +492,25 @@ int ect_matrix_export(ect_matrix* a, int32_t* row_ptr, int32_t* col_idx, double*
     if (values) {
       require(a->assembled, ECT_ERR_SOLVER, "export: matrix values not assembled");
       CK(cudaMemcpyAsync(values, a->val.p, a->nnz * sizeof(double2), cudaMemcpyDefault, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ect_matrix_export_csc(ect_matrix* a, int32_t* col_ptr, int32_t* row_idx, double* values) {
+  return guarded([&] {
+    ect_ctx* ctx = a->ctx;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(a->from_mesh, ECT_ERR_SOLVER,
+            "export_csc: only matrices built from a mesh carry the symmetric pattern");
+    if (col_ptr) CK(cudaMemcpyAsync(col_ptr, a->row_ptr.p, (a->n + 1) * sizeof(int), cudaMemcpyDefault, ctx->stream));
+    if (row_idx) CK(cudaMemcpyAsync(row_idx, a->col.p, a->nnz * sizeof(int), cudaMemcpyDefault, ctx->stream));
+    if (values) {
+      require(a->assembled, ECT_ERR_SOLVER, "export: matrix values not assembled");
+      Out<double2> o(ctx, reinterpret_cast<double2*>(values), a->nnz);
+      ect::export_csc_values(a, o.dev);
+      o.finish();
     }
     CK(cudaStreamSynchronize(ctx->stream));
   });

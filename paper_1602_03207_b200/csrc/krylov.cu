@@ -544,6 +544,20 @@ void compute_jacobi(ect_matrix* a) {
 }
 
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
+  if (k < 1 || k > 16) fail(ECT_ERR_SOLVER, "spmv: n_rhs must be in 1..16");
+  if (k & (k - 1)) {  // pad to the next supported width
+    int kk = 1;
+    while (kk < k) kk <<= 1;
+    DevBuf<double2> xp((size_t)a->n * kk), yp((size_t)a->n * kk);
+    CK(cudaMemsetAsync(xp.p, 0, xp.bytes(), ctx->stream));
+    CK(cudaMemcpy2DAsync(xp.p, kk * sizeof(double2), x, k * sizeof(double2), k * sizeof(double2),
+                         a->n, cudaMemcpyDeviceToDevice, ctx->stream));
+    spmv(ctx, a, xp.p, yp.p, kk);
+    CK(cudaMemcpy2DAsync(y, k * sizeof(double2), yp.p, kk * sizeof(double2), k * sizeof(double2),
+                         a->n, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   with_k(k, [&](auto D) {
     using DK = decltype(D);
     KrylovCtl ctl{};

@@ -156,7 +156,36 @@ __global__ void k_fill_columns(const int* __restrict__ nbr_off, const int* __res
   }
 }
 
+// CSR value order -> the reference's CSC value order. The pattern is
+// symmetric, so the CSC slot of A(i, j) is the position of column i inside
+// row j. Warp per row, binary search per entry; a pure permutation.
+__global__ void k_csr_to_csc(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                             const double2* __restrict__ val, int64_t n, double2* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += n_warps) {
+    for (int p = row_ptr[i] + lane; p < row_ptr[i + 1]; p += 32) {
+      const int j = col[p];
+      int lo = row_ptr[j], hi = row_ptr[j + 1] - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (col[mid] < (int)i) lo = mid + 1; else hi = mid;
+      }
+      out[lo] = val[p];
+    }
+  }
+}
+
 }  // namespace
+
+void export_csc_values(ect_matrix* a, double2* out) {
+  ect_ctx* ctx = a->ctx;
+  k_csr_to_csc<<<blocks_for(ctx, 32 * a->n), 256, 0, ctx->stream>>>(a->row_ptr.p, a->col.p,
+                                                                   a->val.p, a->n, out);
+  CK_LAUNCH();
+  note_launch(ctx, 1);
+}
 
 void build_pattern(ect_mesh* m, ect_matrix* a) {
   ect_ctx* ctx = m->ctx;

@@ -147,6 +147,15 @@ class Context:
     def synchronize(self):
         _check(lib().ect_ctx_synchronize(self.h))
 
+    def mark(self, slot: int):
+        """Record event `slot` on the context stream (device-side timing)."""
+        _check(lib().ect_ctx_mark(self.h, C.c_int(slot)))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = D()
+        _check(lib().ect_ctx_elapsed_ms(self.h, C.c_int(a), C.c_int(b), C.byref(ms)))
+        return ms.value
+
 
 class Mesh:
     """Mesh + ConductorIndexMap + boundary pins, resident on the device."""
@@ -239,6 +248,14 @@ class Matrix:
         v = np.empty(self.nnz, np.complex128) if values else None
         _check(lib().ect_matrix_export(self.h, _ptr(rp), _ptr(ci), _ptr(v)))
         return rp, ci, v
+
+    def export_csc(self):
+        """The reference's CscMatrix arrays of build_global (col_ptr, row_idx, values)."""
+        cp = np.empty(self.n + 1, np.int32)
+        ri = np.empty(self.nnz, np.int32)
+        v = np.empty(self.nnz, np.complex128)
+        _check(lib().ect_matrix_export_csc(self.h, _ptr(cp), _ptr(ri), _ptr(v)))
+        return cp, ri, v
 
     def multiply(self, x, out=None):
         """y = A x (CscMatrix::multiply); x is [n] or [n, k] interleaved."""

@@ -66,3 +66,19 @@ def solution_errors(x, x_ref, n_nodes, comp):
 def csr(row_ptr, col, vals):
     n = len(row_ptr) - 1
     return sp.csr_matrix((vals, col, row_ptr), shape=(n, n))
+
+
+def ref_matrix(g, key="primary"):
+    """The reference's CscMatrix (sparse.hpp:55-66) as scipy CSC."""
+    cp = g[f"{key}_col_ptr"]
+    n = len(cp) - 1
+    return sp.csc_matrix((g[f"{key}_values"], g[f"{key}_row_idx"], cp), shape=(n, n))
+
+
+def ref_csr_values(g, key="primary"):
+    """Reference values permuted into CSR order (pure permutation, no arithmetic).
+    The pattern is symmetric, so the CSR index arrays equal the CSC ones."""
+    a = ref_matrix(g, key).tocsr()
+    a.sort_indices()
+    assert np.array_equal(a.indptr, g[f"{key}_col_ptr"])
+    return a.data

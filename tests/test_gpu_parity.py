@@ -8,13 +8,16 @@ fixtures made by oracle/make_golden.py). Bars:
   rhs                            : <= 1e-14 relative (hypot may differ by 1 ulp)
   solution                       : D9 A-part and mean-free V-part rel. L2 <= 1e-6
   impedance                      : |dZ - dZ*| / max|dZ*| <= 1e-6
+Note: the reference stores A in CSC; A is symmetric only up to rounding, so the
+reference value array read as CSR is A^T. Comparisons use the reference
+matrix as CSC (ref_matrix) or permuted into CSR order (ref_csr_values).
 """
 import numpy as np
 import pytest
 
 from paper_1602_03207_b200 import ect, workloads
-from tests.helpers import (SMALL, conductor_components, csr, golden, solution_errors,
-                           value_metrics)
+from tests.helpers import (SMALL, conductor_components, golden, ref_csr_values, ref_matrix,
+                           solution_errors, value_metrics)
 
 pytestmark = pytest.mark.gpu
 
@@ -25,14 +28,14 @@ def _mesh(ctx, g):
     return ect.Mesh(ctx, g["xyz"], g["tets"], g["region"])
 
 
-def _mats(mesh, g, key):
-    p, r, two = mesh.materials(_physics(g))
-    return p if key == "primary" else r
-
-
 def _physics(g):
     has_defect = bool((g["region"] == 2).any())
     return workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0) if has_defect else workloads.Physics()
+
+
+def _configs(g, p, r):
+    keys = ["primary"] + (["reference"] if bool(g["two_configs"]) else [])
+    return list(zip(keys, (p, r)))
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -46,25 +49,30 @@ def test_mesh_prep_matches_reference(ctx, name):
     p, r, two = m.materials(_physics(g))
     assert two == bool(g["two_configs"])
     assert p.mu_tilde == g["mats_primary"][13]                            # harmonic mu_tilde, exact
+    assert m.n_defect == int((g["region"] == 2).sum())
 
 
 @pytest.mark.parametrize("name", SMALL)
 def test_pattern_and_values_bit_exact(ctx, name):
     g = golden(name)
     m = _mesh(ctx, g)
-    keys = ["primary"] + (["reference"] if bool(g["two_configs"]) else [])
     p, r, _ = m.materials(_physics(g))
-    for key, mats in zip(keys, (p, r)):
+    for key, mats in _configs(g, p, r):
         a = ect.Matrix(ctx, m).assemble(mats)
         rp, ci, v = a.export()
         assert np.array_equal(rp, g[f"{key}_col_ptr"]), "row_ptr != reference col_ptr"
         assert np.array_equal(ci, g[f"{key}_row_idx"]), "col_idx != reference row_idx"
-        ref_v = g[f"{key}_values"]
+        ref_v = ref_csr_values(g, key)
         ms, fr, pin_ok = value_metrics(v, ref_v, rp, ci, g["pins"], mats.bc_penalty)
         assert pin_ok
         assert ms <= 1e-12 and fr <= 1e-12, (ms, fr)
         n_diff = int(np.count_nonzero(v.view(np.uint64) != ref_v.view(np.uint64)))
         assert n_diff == 0, f"{n_diff} of {v.size * 2} doubles differ bitwise (max scaled {ms:.2e})"
+        # the reference's own CscMatrix arrays, byte for byte
+        cp2, ri2, v2 = a.export_csc()
+        assert cp2.tobytes() == g[f"{key}_col_ptr"].tobytes()
+        assert ri2.tobytes() == g[f"{key}_row_idx"].tobytes()
+        assert v2.tobytes() == g[f"{key}_values"].tobytes()
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -84,17 +92,18 @@ def test_rhs_matches_reference(ctx, name):
 @pytest.mark.parametrize("name", SMALL)
 def test_spmv_matches_reference_multiply(ctx, name):
     g = golden(name)
-    A = csr(g["primary_col_ptr"], g["primary_row_idx"], g["primary_values"])
+    A = ref_matrix(g).tocsr()
+    A.sort_indices()
+    absA = abs(A)
+    gm = ect.Matrix(ctx, csr=(A.indptr, A.indices, A.data))
     rng = np.random.default_rng(2)
-    for k in (1, 2, 4, 8):
+    for k in (1, 2, 3, 4, 8, 16):
         x = rng.uniform(-1, 1, (A.shape[0], k)) + 1j * rng.uniform(-1, 1, (A.shape[0], k))
         x = np.ascontiguousarray(x if k > 1 else x[:, 0])
-        gm = ect.Matrix(ctx, csr=(g["primary_col_ptr"], g["primary_row_idx"], g["primary_values"]))
         y = gm.multiply(x)
         y_ref = A @ x
-        absA = csr(g["primary_col_ptr"], g["primary_row_idx"], np.abs(g["primary_values"]))
         scale = absA @ np.abs(x)
-        assert np.max(np.abs(y - y_ref) / scale) <= 1e-14
+        assert np.max(np.abs(y - y_ref) / scale) <= 1e-14, k
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -103,8 +112,9 @@ def test_solve_matches_direct_reference(ctx, name):
     m = _mesh(ctx, g)
     comp = conductor_components(g["tets"], g["region"], g["cond_forward"])
     p, r, two = m.materials(_physics(g))
-    for key, mats in zip(["primary"] + (["reference"] if two else []), (p, r)):
+    for key, mats in _configs(g, p, r):
         a = ect.Matrix(ctx, m).assemble(mats)
+        A = ref_matrix(g, key)
         b = np.ascontiguousarray(g["rhs"].T)
         x, res = a.solve(b, tol=SOLVE_TOL, max_iter=20000)
         for c in range(2):
@@ -112,8 +122,7 @@ def test_solve_matches_direct_reference(ctx, name):
             assert res[c]["residual"] <= SOLVE_TOL
             ea, ev = solution_errors(x[:, c], g[f"{key}_x"][c], m.n_nodes, comp)
             assert ea <= 1e-6 and ev <= 1e-6, (key, c, ea, ev)
-            # true residual recomputed on the host from the reference matrix
-            A = csr(g[f"{key}_col_ptr"], g[f"{key}_row_idx"], g[f"{key}_values"])
+            # true residual recomputed on the host with the reference matrix
             rr = np.linalg.norm(g["rhs"][c] - A @ x[:, c]) / np.linalg.norm(g["rhs"][c])
             assert rr <= 2 * SOLVE_TOL, rr
 
@@ -139,20 +148,58 @@ def test_delta_impedance_and_session(ctx, name):
     assert abs(pt["z_f3"] - zf3) / max(abs(zf3), abs(zfa)) <= 1e-6
 
 
+def test_session_null_scan_without_defect(ctx):
+    """test_scan.cpp:65-75: defect-free scan is an exact null."""
+    g = golden("small_5x5x10_nodefect")
+    m = _mesh(ctx, g)
+    s = ect.Session(ctx, m, _physics(g), tuple(g["coil"]), float(g["amplitude"]), tol=1e-10)
+    pts = s.solve_positions([float(g["z"])] * 3, positions_per_batch=2)
+    for pt in pts:
+        assert not pt["failed"]
+        assert np.all(pt["dz"] == 0) and pt["z_fa"] == 0 and pt["z_f3"] == 0
+
+
+def test_session_batching_invariance(ctx):
+    """Worker/batch invariance (test_scan.cpp:77-92): positions solved one at a
+    time or batched give the same signals to solver tolerance."""
+    g = golden("small_6x6x12")
+    m = _mesh(ctx, g)
+    s = ect.Session(ctx, m, _physics(g), tuple(g["coil"]), float(g["amplitude"]), tol=1e-11,
+                    max_iter=20000)
+    z0 = float(g["z"])
+    zs = [z0 - 0.0017, z0, z0 + 0.0013]
+    one = s.solve_positions(zs, positions_per_batch=1)
+    many = s.solve_positions(zs, positions_per_batch=4)
+    for a, b in zip(one, many):
+        assert not a["failed"] and not b["failed"]
+        assert np.max(np.abs(a["dz"] - b["dz"])) <= 1e-7 * np.max(np.abs(a["dz"]))
+    again = s.solve_positions(zs, positions_per_batch=1)
+    assert all(np.array_equal(a["dz"], b["dz"]) for a, b in zip(one, again))  # repeatable
+
+
 def test_solver_contracts(ctx):
     """iterative.cpp contracts: b = 0 -> x = 0 converged; tol <= 0 rejected;
     max_iter = 1 reports non-convergence; bitwise-repeatable solves."""
     g = golden("small_4x4x8")
-    a = ect.Matrix(ctx, csr=(g["primary_col_ptr"], g["primary_row_idx"], g["primary_values"]))
+    A = ref_matrix(g).tocsr()
+    A.sort_indices()
+    a = ect.Matrix(ctx, csr=(A.indptr, A.indices, A.data))
     x, res = a.solve(np.zeros(a.n, np.complex128))
     assert res[0]["converged"] and res[0]["iterations"] == 0 and np.all(x == 0)
     with pytest.raises(ect.SolverError):
         a.solve(g["rhs"][0], tol=0.0)
     x1, r1 = a.solve(g["rhs"][0], tol=1e-14, max_iter=1)
-    assert not r1[0]["converged"] and r1[0]["residual"] > 1e-14
+    assert not r1[0]["converged"] and r1[0]["residual"] > 1e-14 and r1[0]["iterations"] == 1
     xa, _ = a.solve(g["rhs"][0], tol=1e-10, max_iter=5000)
     xb, _ = a.solve(g["rhs"][0], tol=1e-10, max_iter=5000)
     assert xa.tobytes() == xb.tobytes()
+    # identity converges in one iteration (test_solver.cpp:196-204)
+    n = 8
+    eye = ect.Matrix(ctx, csr=(np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                              np.ones(n, np.complex128)))
+    b = np.arange(1, n + 1) * (1 + 0.5j)
+    xi, ri = eye.solve(b, tol=1e-10, max_iter=50)
+    assert ri[0]["converged"] and ri[0]["iterations"] == 1 and np.allclose(xi, b, rtol=0, atol=1e-12)
 
 
 def test_error_paths(ctx):
@@ -162,9 +209,15 @@ def test_error_paths(ctx):
         m.rhs((10.0, 11.0, 1e-3, 0.0), [float(g["z"])], [1], 1.0)
     with pytest.raises(ect.MeshError):  # support reaching into the conductor slab
         m.rhs((0.0, 1.0, 1.0, 0.0), [float(g["z"])], [1], 1.0)
+    with pytest.raises(ect.MeshError):  # coil index
+        m.rhs(tuple(g["coil"]), [float(g["z"])], [3], 1.0)
     tets = g["tets"].copy()
     tets[0, 3] = tets[0, 2]  # degenerate tet
     with pytest.raises(ect.MeshError):
         ect.Mesh(ctx, g["xyz"], tets, g["region"])
     with pytest.raises(ect.MeshError):  # all vacuum: no conductor dofs
         ect.Mesh(ctx, g["xyz"], g["tets"], np.full_like(g["region"], 5))
+    p, r, _ = m.materials(_physics(g))
+    p.ibc_enabled = 1
+    with pytest.raises(ect.ConfigError):  # IBC surface terms are out of scope
+        ect.Matrix(ctx, m).assemble(p)
