@@ -134,11 +134,12 @@ def make_cfg1():
     out = {"n_nodes": rm.n_nodes, "n_tets": rm.n_tets, "n_cond": rm.n_cond, "two_configs": two,
            "mu_tilde": prim.mu_tilde, "cond_forward_sha": sha(rm.export()["cond_forward"])}
     for tag, mats in (("primary", prim), ("reference", refm)):
-        s = ref.RefSystem(rm, mats, parts=8, workers=8)
+        # parts = 1: the summation order the GPU reproduces bit for bit
+        s = ref.RefSystem(rm, mats, parts=1, workers=1)
         col_ptr, row_idx, vals, pins = s.export()
         out[tag] = {"n": int(len(col_ptr) - 1), "nnz": int(len(row_idx)), "n_pins": int(len(pins)),
                     "sha_col_ptr": sha(col_ptr), "sha_row_idx": sha(row_idx),
-                    "frob": float(np.linalg.norm(vals)),
+                    "sha_values": sha(vals), "frob": float(np.linalg.norm(vals)),
                     "timings_s": {k: float(v) for k, v in s.timings.items()}}
         out["pins_sha"] = sha(np.sort(pins))
         del s, col_ptr, row_idx, vals

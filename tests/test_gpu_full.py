@@ -1,0 +1,97 @@
+"""Full-size BASELINE configs on the GPU vs the reference.
+
+configs[0] (20x20x40): pattern, pins, conductor map and VALUES bit-exact against
+the reference's CscMatrix (sha256 of the arrays the reference build produced,
+tests/golden/cfg0.npz); solutions of both coil right-hand sides within 1e-6
+(D9 metrics) of the reference GMRES(80)+ILU(0) solution at tol 1e-12.
+configs[1] (64x64x128): pattern/values sha256 against the reference build
+(tests/golden/cfg1.json, parts = 1), plus size-independent properties of the
+solve (true residual recomputed on the host, complex symmetry of A).
+"""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from paper_1602_03207_b200 import ect, workloads
+from tests.helpers import GOLDEN, conductor_components, solution_errors
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def cfg0(ctx):
+    w = workloads.config0()
+    m = w.mesh()
+    mesh = ect.Mesh(ctx, m.xyz, m.tets, m.region)
+    return w, m, mesh
+
+
+def test_cfg0_bit_exact_against_reference(ctx, cfg0):
+    w, m, mesh = cfg0
+    g = np.load(GOLDEN / "cfg0.npz")
+    ex = mesh.export()
+    assert sha(ex["cond_forward"]) == str(g["cond_forward_sha"])
+    assert sha(ex["pinned_dofs"]) == str(g["pins_sha"])
+    p, r, two = mesh.materials(w.physics)
+    assert not two  # no deposit: one configuration, dZ == 0 (scan.cpp:49)
+    a = ect.Matrix(ctx, mesh).assemble(p)
+    assert a.n == int(g["n"]) and a.nnz == int(g["nnz"])
+    cp, ri, v = a.export_csc()
+    assert sha(cp) == str(g["sha_col_ptr"])
+    assert sha(ri) == str(g["sha_row_idx"])
+    assert sha(v) == str(g["sha_values"]), "configs[0] values differ from the reference bitwise"
+
+
+def test_cfg0_solution_matches_reference_gmres(ctx, cfg0):
+    w, m, mesh = cfg0
+    g = np.load(GOLDEN / "cfg0.npz")
+    p, r, two = mesh.materials(w.physics)
+    a = ect.Matrix(ctx, mesh).assemble(p)
+    b = mesh.rhs(w.coil, [w.positions[0]] * 2, [1, 2], w.amplitude)
+    assert np.max(np.abs(b - g["rhs"].T)) <= 1e-14 * np.max(np.abs(g["rhs"]))
+    fwd = mesh.export()["cond_forward"]
+    comp = conductor_components(m.tets, m.region, fwd)
+    for tol in (1e-8, 1e-10):
+        x, res = a.solve(b, tol=tol, max_iter=20000)
+        for c in range(2):
+            assert res[c]["converged"] and res[c]["residual"] <= tol
+            ea, ev = solution_errors(x[:, c], g["x"][c], m.n_nodes, comp)
+            # tol 1e-8 is the BASELINE tolerance; SURVEY D9 observed 2.5e-9
+            assert ea <= 1e-6 and ev <= 1e-6, (tol, c, ea, ev)
+
+
+def test_cfg1_bit_exact_and_solve_properties(ctx):
+    w = workloads.config1()
+    m = w.mesh()
+    mesh = ect.Mesh(ctx, m.xyz, m.tets, m.region)
+    gold = json.loads((GOLDEN / "cfg1.json").read_text())
+    assert mesh.n_cond == gold["n_cond"]
+    assert sha(mesh.export()["cond_forward"]) == gold["cond_forward_sha"]
+    p, r, two = mesh.materials(w.physics)
+    assert two and p.mu_tilde == gold["mu_tilde"]
+    for key, mats in (("primary", p), ("reference", r)):
+        a = ect.Matrix(ctx, mesh).assemble(mats)
+        cp, ri, v = a.export_csc()
+        assert a.n == gold[key]["n"] and a.nnz == gold[key]["nnz"]
+        assert sha(cp) == gold[key]["sha_col_ptr"] and sha(ri) == gold[key]["sha_row_idx"]
+        if "sha_values" in gold[key]:
+            assert sha(v) == gold[key]["sha_values"], f"{key} values differ bitwise"
+        assert abs(np.linalg.norm(v) - gold[key]["frob"]) <= 1e-13 * gold[key]["frob"]
+    # solve: true residual on the host, complex symmetry A = A^T
+    import scipy.sparse as sp
+    a = ect.Matrix(ctx, mesh).assemble(p)
+    rp, ci, vals = a.export()
+    A = sp.csr_matrix((vals, ci, rp), shape=(a.n, a.n))
+    asym = abs(A - A.T).max() / abs(A).max()
+    assert asym <= 1e-15
+    b = mesh.rhs(w.coil, [w.positions[0]], [1], w.amplitude)[:, 0]
+    x, res = a.solve(b, tol=1e-8, max_iter=20000)
+    assert res[0]["converged"]
+    rr = np.linalg.norm(b - A @ x) / np.linalg.norm(b)
+    assert rr <= 1e-8 * 1.01, rr
