@@ -130,6 +130,16 @@ int ect_ctx_timings(ect_ctx* ctx, ect_timings* out, int reset);
  * iteration; used by bench.py for the roofline figure). */
 int ect_ctx_set_profiling(ect_ctx* ctx, int enabled);
 int ect_ctx_synchronize(ect_ctx* ctx);
+/* SpMV storage for matrices assembled on this context afterwards:
+ * ECT_FORMAT_NB (default: node-block, 3x3 real blocks + diagonal imaginary
+ * parts + real couplings) or ECT_FORMAT_CSR (plain complex CSR). Both give
+ * the same matrix; NB moves ~40% fewer bytes per SpMV (configs[2]'s
+ * storage comparison). */
+#define ECT_FORMAT_NB 0
+#define ECT_FORMAT_CSR 1
+int ect_ctx_set_format(ect_ctx* ctx, int format);
+/* 1 when m uses the NB SpMV format, 0 for CSR. */
+int ect_matrix_format(ect_matrix* m, int32_t* nb);
 /* Device-side timing on the context stream: record event `slot` (0..7), and
  * the elapsed ms between two recorded slots (waits for the later one). */
 int ect_ctx_mark(ect_ctx* ctx, int slot);

@@ -99,6 +99,7 @@ struct ect_ctx {
   int* pinned_flag = nullptr;  // small pinned word for convergence polling
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
+  bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
 };
 
 struct ect_mesh {
@@ -135,6 +136,19 @@ struct ect_matrix {
   ect::DevBuf<int> col;
   ect::DevBuf<double2> val;
   ect::DevBuf<double2> dinv;       // Jacobi preconditioner 1/diag
+  // Node-block (NB) streaming format for the SpMV (krylov.cu, build_nb):
+  // per node i, 3x3 A-A blocks (real parts + the 3 diagonal imaginary parts,
+  // 6 double2 planes) over the neighbour list, and conductor couplings
+  // (A-V column, V-A row, V-V entry: 4 double2 planes).
+  bool has_nb = false;
+  int64_t nb_blocks = 0, nb_ncpl = 0;
+  const int* nb_blk_ptr = nullptr;  // = mesh->nbr_off (borrowed)
+  const int* nb_blk_col = nullptr;  // = mesh->nbr (borrowed)
+  const int* nb_cond_fwd = nullptr; // = mesh->cond_fwd (borrowed)
+  ect::DevBuf<double2> nb_blk;      // [6][nb_blocks]
+  ect::DevBuf<int> nb_cpl_ptr;      // n_nodes + 1
+  ect::DevBuf<int2> nb_cpl_idx;     // (node m, cond dof of m)
+  ect::DevBuf<double2> nb_cpl;      // [4][nb_cpl]
 };
 
 namespace ect {
@@ -148,6 +162,7 @@ void build_pattern(ect_mesh* m, ect_matrix* a);                // pattern.cu
 void export_csc_values(ect_matrix* a, double2* out);           // pattern.cu (symmetric pattern)
 void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a);  // assembly.cu
 void compute_jacobi(ect_matrix* a);                            // krylov.cu
+void build_nb(ect_mesh* m, ect_matrix* a);                     // krylov.cu (NB format)
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k);  // spmv.cu
 void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* which, int n_rhs,
                double amplitude, double2* rhs);                // rhs.cu

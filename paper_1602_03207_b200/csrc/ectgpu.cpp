@@ -231,6 +231,19 @@ int ect_ctx_set_profiling(ect_ctx* ctx, int enabled) {
   });
 }
 
+int ect_ctx_set_format(ect_ctx* ctx, int format) {
+  return guarded([&] {
+    require(format == ECT_FORMAT_NB || format == ECT_FORMAT_CSR, ECT_ERR_CONFIG,
+            "ect_ctx_set_format: unknown format");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx->force_csr = format == ECT_FORMAT_CSR;
+  });
+}
+
+int ect_matrix_format(ect_matrix* m, int32_t* nb) {
+  return guarded([&] { *nb = m->has_nb ? 1 : 0; });
+}
+
 int ect_ctx_mark(ect_ctx* ctx, int slot) {
   return guarded([&] {
     require(slot >= 0 && slot < 8, ECT_ERR_OTHER, "ect_ctx_mark: slot must be in 0..7");

@@ -246,6 +246,287 @@ k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
   }
 }
 
+// ---- node-block (NB) SpMV ----------------------------------------------------
+// The A–V matrix has exploitable structure: the 3 A-rows of a
+// node share one column set (3x3 blocks), A-A entries are real except the
+// c == d mass entries, and the A-V / V-A couplings are real. NB stores per
+// node i its 3x3 blocks as 12 doubles (9 real + 3 diagonal imaginary) in 6
+// double2 planes (one coalesced 16-byte load per plane per lane), sharing one
+// int32 column per block, and its conductor couplings (AV[3], VA[3], VV) as
+// 4 double2 planes + one int2 (node, V-dof). ~11 B per A-A entry instead of
+// CSR's 20, and each x gather (3 contiguous complex per column node) feeds 3
+// rows. The imaginary parts dropped are exact zeros (checked at build).
+struct NbView {
+  const int* blk_ptr;
+  const int* blk_col;
+  const double2* blk;   // plane p at blk + p * nblk
+  int64_t nblk;
+  const int* cpl_ptr;
+  const int2* cpl_idx;
+  const double2* cpl;   // plane p at cpl + p * ncpl
+  int64_t ncpl;
+  const int* cond_fwd;
+  int64_t n_nodes;
+};
+
+__device__ __forceinline__ int2 ldg_i2(const int2* p) {
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+template <int G, int K, int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
+          const double2* __restrict__ b, KrylovCtl ctl) {
+  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
+  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  bool act[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) act[k] = (MODE == kPlain) || ctl.st[k].status == kActive;
+  constexpr int NPW = 32 / G;  // nodes per warp and pass
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t na = 3 * A.n_nodes;
+  double part[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+
+  for (int64_t wn = warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
+    const int64_t i = wn + lane / G;
+    const bool valid = i < A.n_nodes;
+    double2 acc[3][K], accv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
+    }
+    int cf_i = -1;
+    if (valid) {
+      const int be = A.blk_ptr[i + 1];
+#pragma unroll 2
+      for (int q = A.blk_ptr[i] + g; q < be; q += G) {
+        const int m = ldg_i(A.blk_col + q);
+        const double2 P0 = ldg2(A.blk + q), P1 = ldg2(A.blk + A.nblk + q),
+                      P2 = ldg2(A.blk + 2 * A.nblk + q), P3 = ldg2(A.blk + 3 * A.nblk + q),
+                      P4 = ldg2(A.blk + 4 * A.nblk + q), P5 = ldg2(A.blk + 5 * A.nblk + q);
+        const double B[3][3] = {{P0.x, P0.y, P1.x}, {P1.y, P2.x, P2.y}, {P3.x, P3.y, P4.x}};
+        const double Im[3] = {P4.y, P5.x, P5.y};
+        const double2* xm = x + (int64_t)3 * m * K;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (!act[k]) continue;
+          const double2 x0 = xm[k], x1 = xm[K + k], x2 = xm[2 * K + k];
+          const double2 xs[3] = {x0, x1, x2};
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double2 s = acc[c][k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              s.x += B[c][d] * xs[d].x;
+              s.y += B[c][d] * xs[d].y;
+            }
+            s.x -= Im[c] * xs[c].y;
+            s.y += Im[c] * xs[c].x;
+            acc[c][k] = s;
+          }
+        }
+      }
+      cf_i = A.cond_fwd[i];
+      if (cf_i >= 0) {
+        const int ce = A.cpl_ptr[i + 1];
+        for (int q = A.cpl_ptr[i] + g; q < ce; q += G) {
+          const int2 mi = ldg_i2(A.cpl_idx + q);
+          const double2 Q0 = ldg2(A.cpl + q), Q1 = ldg2(A.cpl + A.ncpl + q),
+                        Q2 = ldg2(A.cpl + 2 * A.ncpl + q), Q3 = ldg2(A.cpl + 3 * A.ncpl + q);
+          const double av[3] = {Q0.x, Q0.y, Q1.x};
+          const double va[3] = {Q1.y, Q2.x, Q2.y};
+          const double2* xm = x + (int64_t)3 * mi.x * K;
+          const double2* xv = x + (na + mi.y) * K;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (!act[k]) continue;
+            const double2 v = xv[k];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              acc[c][k].x += av[c] * v.x;
+              acc[c][k].y += av[c] * v.y;
+            }
+            double2 s = accv[k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double2 xd = xm[d * K + k];
+              s.x += va[d] * xd.x;
+              s.y += va[d] * xd.y;
+            }
+            s.x += Q3.x * v.x - Q3.y * v.y;
+            s.y += Q3.x * v.y + Q3.y * v.x;
+            accv[k] = s;
+          }
+        }
+      }
+    }
+    // segment reduction over the G lanes of a node
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int o = G / 2; o; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
+          acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
+        }
+        accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
+        accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
+      }
+    }
+    if (g == 0 && valid) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c == 3 && cf_i < 0) break;
+          const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
+          const double2 v = c < 3 ? acc[c][k] : accv[k];
+          const int64_t idx = row * K + k;
+          if (MODE == kPlain) {
+            y[idx] = v;
+          } else if (MODE == kCocg) {
+            y[idx] = v;
+            const double2 pv = x[idx];
+            part[2 * k] += pv.x * v.x - pv.y * v.y;
+            part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
+          } else {
+            const double2 rv = csub(b[idx], v);
+            y[idx] = rv;
+            part[k] += rv.x * rv.x + rv.y * rv.y;
+          }
+        }
+      }
+    }
+  }
+  if (MODE == kPlain) return;
+
+  block_sum<NV>(part, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    if (MODE == kCocg) {
+      int active = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        RhsState& s = ctl.st[k];
+        if (s.status != kActive) continue;
+        const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
+        if (pq.x == 0.0 && pq.y == 0.0) {
+          s.status = kBreakdown;
+          continue;
+        }
+        s.alpha = cdiv(s.rho, pq);
+        ++active;
+      }
+      *ctl.n_active = active;
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
+// CSR (assembled, node-structured) -> NB planes. Warp per node; lane = block.
+__global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __restrict__ val,
+                           const int* __restrict__ nbr_off, const int* __restrict__ nbr,
+                           const uint8_t* __restrict__ nbr_cond, const int* __restrict__ cond_fwd,
+                           const int* __restrict__ cpl_ptr, int64_t n_nodes, double2* blk,
+                           int64_t nblk, int2* cpl_idx, double2* cpl, int64_t ncpl, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t na = 3 * n_nodes;
+  for (int64_t i = warp; i < n_nodes; i += n_warps) {
+    const int nb = nbr_off[i], u = nbr_off[i + 1] - nb;
+    const int cf_i = cond_fwd[i];
+    int ncc = 0;
+    for (int r0 = 0; r0 < u; r0 += 32) {
+      bool c = (r0 + lane < u) && nbr_cond[nb + r0 + lane];
+      ncc += __popc(__ballot_sync(0xffffffffu, c));
+    }
+    const int base[3] = {row_ptr[3 * i], row_ptr[3 * i + 1], row_ptr[3 * i + 2]};
+    const int basev = cf_i >= 0 ? row_ptr[na + cf_i] : 0;
+    const int cb = cpl_ptr[i];
+    int rc0 = 0;
+    for (int r0 = 0; r0 < u; r0 += 32) {
+      const int r = r0 + lane;
+      const bool valid = r < u;
+      const bool mc = valid && nbr_cond[nb + r];
+      const unsigned mask = __ballot_sync(0xffffffffu, mc);
+      const int rc = rc0 + __popc(mask & ((1u << lane) - 1u));
+      rc0 += __popc(mask);
+      if (!valid) continue;
+      double Bv[3][3], Im[3];
+      int nonzero_offdiag_im = 0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double2 v = val[base[c] + 3 * r + d];
+          Bv[c][d] = v.x;
+          if (c == d) Im[c] = v.y; else nonzero_offdiag_im |= v.y != 0.0;
+        }
+      const int64_t q = nb + r;
+      blk[q] = make_double2(Bv[0][0], Bv[0][1]);
+      blk[nblk + q] = make_double2(Bv[0][2], Bv[1][0]);
+      blk[2 * nblk + q] = make_double2(Bv[1][1], Bv[1][2]);
+      blk[3 * nblk + q] = make_double2(Bv[2][0], Bv[2][1]);
+      blk[4 * nblk + q] = make_double2(Bv[2][2], Im[0]);
+      blk[5 * nblk + q] = make_double2(Im[1], Im[2]);
+      if (mc) {
+        const int m = nbr[nb + r];
+        const int64_t p = cb + rc;
+        double av[3], va[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double2 v = val[base[c] + 3 * u + rc];
+          av[c] = v.x;
+          nonzero_offdiag_im |= v.y != 0.0;
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double2 v = val[basev + 3 * rc + d];
+          va[d] = v.x;
+          nonzero_offdiag_im |= v.y != 0.0;
+        }
+        const double2 vv = val[basev + 3 * ncc + rc];
+        cpl_idx[p] = make_int2(m, cond_fwd[m]);
+        cpl[p] = make_double2(av[0], av[1]);
+        cpl[ncpl + p] = make_double2(av[2], va[0]);
+        cpl[2 * ncpl + p] = make_double2(va[1], va[2]);
+        cpl[3 * ncpl + p] = vv;
+      }
+      if (nonzero_offdiag_im) atomicOr(bad, 1);
+    }
+  }
+}
+
+__global__ void k_cpl_count(const int* __restrict__ nbr_off, const uint8_t* __restrict__ nbr_cond,
+                            const int* __restrict__ cond_fwd, int64_t n_nodes, int* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    if (cond_fwd[i] >= 0)
+      for (int p = nbr_off[i]; p < nbr_off[i + 1]; ++p) c += nbr_cond[p];
+    cnt[i] = c;
+  }
+}
+
 // x += alpha p ; r -= alpha q ; z = D^-1 r ; partial r^T z, ||r||^2
 // last block: convergence test, beta, rho.
 template <int K>
@@ -440,11 +721,32 @@ struct Launch {
   int grid_spmv = 0, grid_vec = 0;
 };
 
+NbView nb_view(const ect_matrix* a) {
+  return NbView{a->nb_blk_ptr, a->nb_blk_col, a->nb_blk.p, a->nb_blocks, a->nb_cpl_ptr.p,
+                a->nb_cpl_idx.p, a->nb_cpl.p, a->nb_ncpl, a->nb_cond_fwd, a->n_nodes};
+}
+
+constexpr int kNbG = 8;  // lanes per node in the NB SpMV
+
 template <int K>
 struct Dispatch {
+  static constexpr bool kNbOk = K <= 8;
   static void spmv(ect_ctx* ctx, int mode, int grid, int64_t n, const ect_matrix* a,
                    const double2* x, double2* y, const double2* b, KrylovCtl ctl) {
     cudaStream_t s = ctx->stream;
+    if constexpr (kNbOk) {
+      if (a->has_nb) {
+        const NbView v = nb_view(a);
+        if (mode == kPlain)
+          k_nb_spmv<kNbG, K, kPlain><<<grid, kBlock, 0, s>>>(v, x, y, b, ctl);
+        else if (mode == kCocg)
+          k_nb_spmv<kNbG, K, kCocg><<<grid, kBlock, 0, s>>>(v, x, y, b, ctl);
+        else
+          k_nb_spmv<kNbG, K, kResid><<<grid, kBlock, 0, s>>>(v, x, y, b, ctl);
+        CK_LAUNCH();
+        return;
+      }
+    }
     constexpr int G = K >= 4 ? 8 : 16;
     if (mode == kPlain)
       k_spmv<G, K, kPlain><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
@@ -469,7 +771,15 @@ struct Dispatch {
     k_start<K><<<grid, kBlock, 0, ctx->stream>>>(n, b, x, r, p, dinv, mask, fresh, ctl);
     CK_LAUNCH();
   }
-  static int spmv_grid(ect_ctx* ctx, int mode) {
+  static int spmv_grid(ect_ctx* ctx, int mode, const ect_matrix* a) {
+    if constexpr (kNbOk) {
+      if (a->has_nb) {
+        const void* f = mode == kPlain  ? (const void*)k_nb_spmv<kNbG, K, kPlain>
+                        : mode == kCocg ? (const void*)k_nb_spmv<kNbG, K, kCocg>
+                                        : (const void*)k_nb_spmv<kNbG, K, kResid>;
+        return grid_for(ctx, f, kBlock);
+      }
+    }
     constexpr int G = K >= 4 ? 8 : 16;
     const void* f = mode == kPlain  ? (const void*)k_spmv<G, K, kPlain>
                     : mode == kCocg ? (const void*)k_spmv<G, K, kCocg>
@@ -543,6 +853,60 @@ void compute_jacobi(ect_matrix* a) {
   (void)h;  // zero diagonals fall back to identity scaling (reported by the solve if singular)
 }
 
+void build_nb(ect_mesh* m, ect_matrix* a) {
+  ect_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  a->has_nb = false;
+  const int64_t nn = m->n_nodes;
+  int64_t nblk = 0;
+  {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, m->nbr_off.p + nn, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nblk = h;
+  }
+  DevBuf<int> cnt(nn + 1);
+  CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), s));
+  const int grid = (int)std::min<int64_t>((nn + 255) / 256, (int64_t)ctx->num_sms * 16);
+  k_cpl_count<<<std::max(grid, 1), 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p, m->cond_fwd.p, nn,
+                                                 cnt.p);
+  CK_LAUNCH();
+  a->nb_cpl_ptr.alloc(nn + 1);
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.p, a->nb_cpl_ptr.p, nn + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, cnt.p, a->nb_cpl_ptr.p, nn + 1, s));
+  int ncpl = 0;
+  CK(cudaMemcpyAsync(&ncpl, a->nb_cpl_ptr.p + nn, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  a->nb_blocks = nblk;
+  a->nb_ncpl = ncpl;
+  a->nb_blk.alloc(6 * std::max<int64_t>(1, nblk));
+  a->nb_cpl_idx.alloc(std::max(1, ncpl));
+  a->nb_cpl.alloc(4 * (size_t)std::max(1, ncpl));
+  a->nb_blk_ptr = m->nbr_off.p;
+  a->nb_blk_col = m->nbr.p;
+  a->nb_cond_fwd = m->cond_fwd.p;
+  DevBuf<int> bad(1);
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  const int wgrid = (int)std::min<int64_t>((32 * nn + 255) / 256, (int64_t)ctx->num_sms * 16);
+  k_build_nb<<<std::max(wgrid, 1), 256, 0, s>>>(a->row_ptr.p, a->val.p, m->nbr_off.p, m->nbr.p,
+                                                 m->nbr_cond.p, m->cond_fwd.p, a->nb_cpl_ptr.p, nn,
+                                                 a->nb_blk.p, nblk, a->nb_cpl_idx.p, a->nb_cpl.p,
+                                                 ncpl, bad.p);
+  CK_LAUNCH();
+  note_launch(ctx, 3);
+  int h_bad = 0;
+  CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // NB drops imaginary parts it proves to be exact zeros; otherwise stay CSR.
+  a->has_nb = h_bad == 0;
+  if (!a->has_nb) {
+    a->nb_blk.release();
+    a->nb_cpl.release();
+    a->nb_cpl_idx.release();
+  }
+}
+
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
   if (k < 1 || k > 16) fail(ECT_ERR_SOLVER, "spmv: n_rhs must be in 1..16");
   if (k & (k - 1)) {  // pad to the next supported width
@@ -561,7 +925,7 @@ void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
   with_k(k, [&](auto D) {
     using DK = decltype(D);
     KrylovCtl ctl{};
-    const int grid = DK::spmv_grid(ctx, kPlain);
+    const int grid = DK::spmv_grid(ctx, kPlain, a);
     cudaEvent_t ev[2];
     prof_begin(ctx, ev);
     DK::spmv(ctx, kPlain, grid, a->n, a, x, y, nullptr, ctl);
@@ -586,8 +950,8 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
 
   with_k(kk, [&](auto D) {
     using DK = decltype(D);
-    const int grid_s = DK::spmv_grid(ctx, kCocg);
-    const int grid_r = DK::spmv_grid(ctx, kResid);
+    const int grid_s = DK::spmv_grid(ctx, kCocg, a);
+    const int grid_r = DK::spmv_grid(ctx, kResid, a);
     const int grid_v = DK::vec_grid(ctx);
     const int grid_max = std::max(std::max(grid_s, grid_r), grid_v);
     const size_t vec = (size_t)n * kk;

@@ -52,29 +52,36 @@ __global__ void k_times4(const int* __restrict__ in, int64_t n, int* out) {
     out[i] = 4 * in[i];
 }
 
-// Per node: number of distinct neighbours and of conductor neighbours.
+// Per node: number of distinct neighbours (the group's last key carries the
+// OR of its conductor bits).
 __global__ void k_count_neighbours(const int* __restrict__ inc_off, const int* __restrict__ cand,
-                                   const int* __restrict__ cond_fwd, int64_t n_nodes,
-                                   int* nbr_cnt, int* row_len) {
-  const int64_t na = 3 * n_nodes;
+                                   int64_t n_nodes, int* nbr_cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
        i += (int64_t)gridDim.x * blockDim.x) {
     int b = 4 * inc_off[i], e = 4 * inc_off[i + 1];
-    int u = 0, cc = 0;
+    int u = 0;
     for (int p = b; p < e; ++p) {
-      int v = cand[p];
-      bool last = (p + 1 == e) || ((cand[p + 1] >> 1) != (v >> 1));
-      if (last) {  // the group's last key carries the OR of its conductor bits
-        ++u;
-        cc += v & 1;
-      }
+      const int v = cand[p];
+      u += (p + 1 == e) || ((cand[p + 1] >> 1) != (v >> 1));
     }
     nbr_cnt[i] = u;
-    int la = 3 * u + cc;
+  }
+}
+
+// Row lengths: A-rows 3u + cc, V-row 4 cc (u neighbours, cc via conductor tets).
+__global__ void k_row_lengths(const int* __restrict__ nbr_off, const uint8_t* __restrict__ nbr_cond,
+                              const int* __restrict__ cond_fwd, int64_t n_nodes, int* row_len) {
+  const int64_t na = 3 * n_nodes;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = nbr_off[i], u = nbr_off[i + 1] - b;
+    int cc = 0;
+    for (int p = b; p < b + u; ++p) cc += nbr_cond[p];
+    const int la = 3 * u + cc;
     row_len[3 * i] = la;
     row_len[3 * i + 1] = la;
     row_len[3 * i + 2] = la;
-    int cf = cond_fwd[i];
+    const int cf = cond_fwd[i];
     if (cf >= 0) row_len[na + cf] = 4 * cc;
   }
 }
@@ -187,13 +194,12 @@ void export_csc_values(ect_matrix* a, double2* out) {
   note_launch(ctx, 1);
 }
 
-void build_pattern(ect_mesh* m, ect_matrix* a) {
+// Mesh-level neighbour structure (once per mesh; matrices borrow it).
+static void build_neighbours(ect_mesh* m) {
   ect_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   const int64_t nn = m->n_nodes, n_inc = 4 * m->n_tets, n_cand = 4 * n_inc;
-  const int64_t N = 3 * nn + m->n_cond;
   if (n_cand >= (1ll << 31)) fail(ECT_ERR_MESH, "pattern build: candidate count exceeds int32");
-
   DevBuf<int> cand(n_cand), cand_sorted(n_cand), seg(nn + 1);
   k_candidates<<<blocks_for(ctx, n_inc), 256, 0, s>>>(m->tets.p, m->region.p, m->inc.p, n_inc,
                                                      cand.p);
@@ -205,24 +211,16 @@ void build_pattern(ect_mesh* m, ect_matrix* a) {
                                         seg.p, seg.p + 1, s));
   CK(cub::DeviceSegmentedSort::SortKeys(cub_scratch(ctx, tmp), tmp, cand.p, cand_sorted.p,
                                         (int)n_cand, (int)nn, seg.p, seg.p + 1, s));
-
-  DevBuf<int> nbr_cnt(nn + 1), row_len(N + 1);
+  DevBuf<int> nbr_cnt(nn + 1);
   CK(cudaMemsetAsync(nbr_cnt.p, 0, nbr_cnt.bytes(), s));
-  CK(cudaMemsetAsync(row_len.p, 0, row_len.bytes(), s));
-  k_count_neighbours<<<blocks_for(ctx, nn), 256, 0, s>>>(m->inc_off.p, cand_sorted.p,
-                                                        m->cond_fwd.p, nn, nbr_cnt.p, row_len.p);
+  k_count_neighbours<<<blocks_for(ctx, nn), 256, 0, s>>>(m->inc_off.p, cand_sorted.p, nn,
+                                                        nbr_cnt.p);
   CK_LAUNCH();
   m->nbr_off.alloc(nn + 1);
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nbr_cnt.p, m->nbr_off.p, nn + 1, s));
   CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, nbr_cnt.p, m->nbr_off.p, nn + 1, s));
-  int total_nbr = 0;
+  int total_nbr = 0, max_nbr = 0;
   CK(cudaMemcpyAsync(&total_nbr, m->nbr_off.p + nn, sizeof(int), cudaMemcpyDeviceToHost, s));
-  DevBuf<long long> rp64(N + 1);
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, row_len.p, rp64.p, N + 1, s));
-  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, row_len.p, rp64.p, N + 1, s));
-  long long nnz = 0;
-  CK(cudaMemcpyAsync(&nnz, rp64.p + N, sizeof(long long), cudaMemcpyDeviceToHost, s));
-  int max_nbr = 0;
   {
     DevBuf<int> mx(1);
     CK(cub::DeviceReduce::Max(nullptr, tmp, nbr_cnt.p, mx.p, nn, s));
@@ -230,17 +228,37 @@ void build_pattern(ect_mesh* m, ect_matrix* a) {
     CK(cudaMemcpyAsync(&max_nbr, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }
-  if (nnz >= (1ll << 31)) fail(ECT_ERR_MESH, "pattern build: nnz exceeds int32 row pointers");
-
   m->nbr.alloc(std::max(1, total_nbr));
   m->nbr_cond.alloc(std::max(1, total_nbr));
   k_write_neighbours<<<blocks_for(ctx, nn), 256, 0, s>>>(m->inc_off.p, cand_sorted.p,
                                                         m->nbr_off.p, nn, m->nbr.p,
                                                         m->nbr_cond.p);
   CK_LAUNCH();
+  note_launch(ctx, 5);
+  CK(cudaStreamSynchronize(s));
   m->have_nbr = true;
   m->max_nbr = max_nbr;
+}
 
+void build_pattern(ect_mesh* m, ect_matrix* a) {
+  ect_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  if (!m->have_nbr) build_neighbours(m);
+  const int64_t nn = m->n_nodes;
+  const int64_t N = 3 * nn + m->n_cond;
+  DevBuf<int> row_len(N + 1);
+  CK(cudaMemsetAsync(row_len.p, 0, row_len.bytes(), s));
+  k_row_lengths<<<blocks_for(ctx, nn), 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p, m->cond_fwd.p,
+                                                   nn, row_len.p);
+  CK_LAUNCH();
+  size_t tmp = 0;
+  DevBuf<long long> rp64(N + 1);
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, row_len.p, rp64.p, N + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, row_len.p, rp64.p, N + 1, s));
+  long long nnz = 0;
+  CK(cudaMemcpyAsync(&nnz, rp64.p + N, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (nnz >= (1ll << 31)) fail(ECT_ERR_MESH, "pattern build: nnz exceeds int32 row pointers");
   a->n = N;
   a->nnz = nnz;
   a->n_nodes = nn;
@@ -255,7 +273,7 @@ void build_pattern(ect_mesh* m, ect_matrix* a) {
                                                          m->cond_fwd.p, a->row_ptr.p, nn,
                                                          a->col.p);
   CK_LAUNCH();
-  note_launch(ctx, 7);
+  note_launch(ctx, 4);
   CK(cudaStreamSynchronize(s));
 }
 

@@ -147,6 +147,10 @@ class Context:
     def synchronize(self):
         _check(lib().ect_ctx_synchronize(self.h))
 
+    def set_format(self, fmt: str):
+        """SpMV storage of matrices assembled afterwards: 'nb' (default) or 'csr'."""
+        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1}[fmt])))
+
     def mark(self, slot: int):
         """Record event `slot` on the context stream (device-side timing)."""
         _check(lib().ect_ctx_mark(self.h, C.c_int(slot)))
@@ -241,6 +245,12 @@ class Matrix:
     def assemble(self, mats: Materials):
         _check(lib().ect_matrix_assemble(self.ctx.h, self.mesh.h, C.byref(mats), self.h))
         return self
+
+    @property
+    def format(self) -> str:
+        nb = I32()
+        _check(lib().ect_matrix_format(self.h, C.byref(nb)))
+        return "nb" if nb.value else "csr"
 
     def export(self, values=True):
         rp = np.empty(self.n + 1, np.int32)
