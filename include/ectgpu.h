@@ -119,6 +119,8 @@ typedef struct ect_timings {
   double spmv_ms_total;   /* sum of SpMV kernel durations inside the solve */
   int64_t spmv_launches;
   int64_t kernel_launches;
+  double vec_ms_total;    /* fused vector-update kernels (update + p-update) */
+  int64_t vec_launches;
 } ect_timings;
 
 /* ---- context --------------------------------------------------------- */
@@ -137,8 +139,9 @@ int ect_ctx_synchronize(ect_ctx* ctx);
  * storage comparison). */
 #define ECT_FORMAT_NB 0
 #define ECT_FORMAT_CSR 1
+#define ECT_FORMAT_NB_TILED 2 /* NB + shared-memory x tiles (measured slower on B200) */
 int ect_ctx_set_format(ect_ctx* ctx, int format);
-/* 1 when m uses the NB SpMV format, 0 for CSR. */
+/* 0: CSR, 1: NB untiled, 2: NB with shared-memory x tiles. */
 int ect_matrix_format(ect_matrix* m, int32_t* nb);
 /* Device-side timing on the context stream: record event `slot` (0..7), and
  * the elapsed ms between two recorded slots (waits for the later one). */

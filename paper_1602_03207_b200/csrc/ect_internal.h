@@ -79,6 +79,7 @@ enum RhsStatus : int { kActive = 0, kConverged = 1, kBreakdown = 2, kMaxIter = 3
 struct Profile {
   bool enabled = false;
   std::vector<cudaEvent_t> pool;  // pairs (start, stop)
+  std::vector<int> kinds;          // kind of the pair starting at index i
   size_t used = 0;
   int64_t launches = 0;
 };
@@ -100,6 +101,8 @@ struct ect_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
   bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
+  bool no_tiles = true;                         // NB-T only with ect_ctx_set_format(ECT_FORMAT_NB_TILED)
+  int nb_variant = 0;                           // NB SpMV kernel variant (ECT_NB_VARIANT)
 };
 
 struct ect_mesh {
@@ -149,6 +152,12 @@ struct ect_matrix {
   ect::DevBuf<int> nb_cpl_ptr;      // n_nodes + 1
   ect::DevBuf<int2> nb_cpl_idx;     // (node m, cond dof of m)
   ect::DevBuf<double2> nb_cpl;      // [4][nb_cpl]
+  // NB-T: tiles of consecutive nodes with a staged x footprint
+  bool has_nbt = false;
+  int64_t nbt_tiles = 0;
+  int nbt_fmax = 0;
+  ect::DevBuf<int> nbt_fp_off, nbt_fp_node;
+  ect::DevBuf<uint16_t> nbt_lcol, nbt_cpl_lcol;
 };
 
 namespace ect {

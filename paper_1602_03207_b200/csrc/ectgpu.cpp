@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numbers>
@@ -191,6 +192,7 @@ int ect_ctx_create(int device, ect_ctx** out) {
                                   prop.name);
     }
     ctx->num_sms = prop.multiProcessorCount;
+    if (const char* v = std::getenv("ECT_NB_VARIANT")) ctx->nb_variant = std::atoi(v);
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev_a));
     CK(cudaEventCreate(&ctx->ev_b));
@@ -233,15 +235,17 @@ int ect_ctx_set_profiling(ect_ctx* ctx, int enabled) {
 
 int ect_ctx_set_format(ect_ctx* ctx, int format) {
   return guarded([&] {
-    require(format == ECT_FORMAT_NB || format == ECT_FORMAT_CSR, ECT_ERR_CONFIG,
-            "ect_ctx_set_format: unknown format");
+    require(format == ECT_FORMAT_NB || format == ECT_FORMAT_CSR ||
+                format == ECT_FORMAT_NB_TILED,
+            ECT_ERR_CONFIG, "ect_ctx_set_format: unknown format");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ctx->force_csr = format == ECT_FORMAT_CSR;
+    ctx->no_tiles = format != ECT_FORMAT_NB_TILED;
   });
 }
 
 int ect_matrix_format(ect_matrix* m, int32_t* nb) {
-  return guarded([&] { *nb = m->has_nb ? 1 : 0; });
+  return guarded([&] { *nb = m->has_nb ? (m->has_nbt ? 2 : 1) : 0; });
 }
 
 int ect_ctx_mark(ect_ctx* ctx, int slot) {

@@ -250,24 +250,72 @@ k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
 // The A–V matrix has exploitable structure: the 3 A-rows of a
 // node share one column set (3x3 blocks), A-A entries are real except the
 // c == d mass entries, and the A-V / V-A couplings are real. NB stores per
-// node i its 3x3 blocks as 12 doubles (9 real + 3 diagonal imaginary) in 6
-// double2 planes (one coalesced 16-byte load per plane per lane), sharing one
-// int32 column per block, and its conductor couplings (AV[3], VA[3], VV) as
-// 4 double2 planes + one int2 (node, V-dof). ~11 B per A-A entry instead of
-// CSR's 20, and each x gather (3 contiguous complex per column node) feeds 3
-// rows. The imaginary parts dropped are exact zeros (checked at build).
+// node i its 3x3 blocks as 12 doubles (9 real + 3 diagonal imaginary) in 3
+// planes of 4 doubles — one coalesced 256-bit load (LDG.E.ENL2.256, sm_100)
+// per plane per lane — sharing one int32 column per block, and its conductor
+// couplings (AV[3], VA[3], VV) as 2 planes of 4 doubles + one int2 (node,
+// V-dof). ~11 B per A-A entry instead of CSR's 20, and each x gather (3
+// contiguous complex per column node, 256-bit loads for even k) feeds 3 rows.
+// The imaginary parts dropped are exact zeros (checked at build).
 struct NbView {
   const int* blk_ptr;
   const int* blk_col;
-  const double2* blk;   // plane p at blk + p * nblk
+  const double* blk;    // plane p of block q at blk + 4 * (p * nblk + q)
   int64_t nblk;
   const int* cpl_ptr;
   const int2* cpl_idx;
-  const double2* cpl;   // plane p at cpl + p * ncpl
+  const double* cpl;    // plane p of coupling q at cpl + 4 * (p * ncpl + q)
   int64_t ncpl;
   const int* cond_fwd;
   int64_t n_nodes;
 };
+
+// 256-bit streaming load (read-once matrix data: no L1 allocation)
+__device__ __forceinline__ void ld4s(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+// 256-bit read-only load that may allocate in L1 (x gathers are reused)
+__device__ __forceinline__ void ld4x(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+               : "l"(p));
+}
+
+__device__ __forceinline__ void load_block(const NbView& A, int64_t q, double (&B)[3][3],
+                                           double (&Im)[3]) {
+  double v0[4], v1[4], v2[4];
+  ld4s(A.blk + 4 * q, v0);
+  ld4s(A.blk + 4 * (A.nblk + q), v1);
+  ld4s(A.blk + 4 * (2 * A.nblk + q), v2);
+  B[0][0] = v0[0]; B[0][1] = v0[1]; B[0][2] = v0[2];
+  B[1][0] = v0[3]; B[1][1] = v1[0]; B[1][2] = v1[1];
+  B[2][0] = v1[2]; B[2][1] = v1[3]; B[2][2] = v2[0];
+  Im[0] = v2[1]; Im[1] = v2[2]; Im[2] = v2[3];
+}
+
+__device__ __forceinline__ void load_cpl(const NbView& A, int64_t q, double (&av)[3],
+                                         double (&va)[3], double2& vv) {
+  double c0[4], c1[4];
+  ld4s(A.cpl + 4 * q, c0);
+  ld4s(A.cpl + 4 * (A.ncpl + q), c1);
+  av[0] = c0[0]; av[1] = c0[1]; av[2] = c0[2];
+  va[0] = c0[3]; va[1] = c1[0]; va[2] = c1[1];
+  vv = make_double2(c1[2], c1[3]);
+}
+
+// K consecutive complex values (one node component, all right-hand sides).
+template <int K>
+__device__ __forceinline__ void load_xk(const double2* p, double2 (&v)[K]) {
+  if constexpr (K % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < K; j += 2) ld4x(p + j, v[j], v[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) v[j] = __ldg(p + j);
+  }
+}
 
 __device__ __forceinline__ int2 ldg_i2(const int2* p) {
   int2 v;
@@ -275,8 +323,8 @@ __device__ __forceinline__ int2 ldg_i2(const int2* p) {
   return v;
 }
 
-template <int G, int K, int MODE>
-__global__ void __launch_bounds__(kBlock)
+template <int G, int K, int MODE, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB)
 k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           const double2* __restrict__ b, KrylovCtl ctl) {
   constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
@@ -306,20 +354,37 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
     int cf_i = -1;
     if (valid) {
       const int be = A.blk_ptr[i + 1];
-#pragma unroll 2
-      for (int q = A.blk_ptr[i] + g; q < be; q += G) {
-        const int m = ldg_i(A.blk_col + q);
-        const double2 P0 = ldg2(A.blk + q), P1 = ldg2(A.blk + A.nblk + q),
-                      P2 = ldg2(A.blk + 2 * A.nblk + q), P3 = ldg2(A.blk + 3 * A.nblk + q),
-                      P4 = ldg2(A.blk + 4 * A.nblk + q), P5 = ldg2(A.blk + 5 * A.nblk + q);
-        const double B[3][3] = {{P0.x, P0.y, P1.x}, {P1.y, P2.x, P2.y}, {P3.x, P3.y, P4.x}};
-        const double Im[3] = {P4.y, P5.x, P5.y};
+      // software pipeline: the next block's column and planes are in flight
+      // while this block's x gathers and FMAs run (latency-bound otherwise)
+      int q = A.blk_ptr[i] + g;
+      int m_nx = 0;
+      double B_nx[3][3], Im_nx[3];
+      if (q < be) {
+        m_nx = ldg_i(A.blk_col + q);
+        load_block(A, q, B_nx, Im_nx);
+      }
+      for (; q < be; q += G) {
+        const int m = m_nx;
+        double B[3][3], Im[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          Im[c] = Im_nx[c];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
+        }
+        if (q + G < be) {
+          m_nx = ldg_i(A.blk_col + q + G);
+          load_block(A, q + G, B_nx, Im_nx);
+        }
         const double2* xm = x + (int64_t)3 * m * K;
+        double2 xk[3][K];
+        load_xk<K>(xm, xk[0]);
+        load_xk<K>(xm + K, xk[1]);
+        load_xk<K>(xm + 2 * K, xk[2]);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           if (!act[k]) continue;
-          const double2 x0 = xm[k], x1 = xm[K + k], x2 = xm[2 * K + k];
-          const double2 xs[3] = {x0, x1, x2};
+          const double2 xs[3] = {xk[0][k], xk[1][k], xk[2][k]};
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             double2 s = acc[c][k];
@@ -339,16 +404,16 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
         const int ce = A.cpl_ptr[i + 1];
         for (int q = A.cpl_ptr[i] + g; q < ce; q += G) {
           const int2 mi = ldg_i2(A.cpl_idx + q);
-          const double2 Q0 = ldg2(A.cpl + q), Q1 = ldg2(A.cpl + A.ncpl + q),
-                        Q2 = ldg2(A.cpl + 2 * A.ncpl + q), Q3 = ldg2(A.cpl + 3 * A.ncpl + q);
-          const double av[3] = {Q0.x, Q0.y, Q1.x};
-          const double va[3] = {Q1.y, Q2.x, Q2.y};
+          double av[3], va[3];
+          double2 Q3;
+          load_cpl(A, q, av, va, Q3);
           const double2* xm = x + (int64_t)3 * mi.x * K;
-          const double2* xv = x + (na + mi.y) * K;
+          double2 xvk[K];
+          load_xk<K>(x + (na + mi.y) * K, xvk);
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             if (!act[k]) continue;
-            const double2 v = xv[k];
+            const double2 v = xvk[k];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               acc[c][k].x += av[c] * v.x;
@@ -441,12 +506,286 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   }
 }
 
+// ---- tiled NB SpMV with shared-memory x staging (NB-T) -------------------------
+// A CTA owns a tile of kTileW consecutive nodes. The union of their neighbour
+// nodes (the tile's x "footprint", ~7 runs of consecutive node ids on a
+// lexicographically numbered mesh, ~0.5 of the per-block gathers) is staged
+// once into shared memory with coalesced loads; blocks then address x through
+// a 16-bit local column. This replaces ~15 scattered 96-byte x gathers per
+// node (the L1-wavefront bottleneck of the untiled kernel) by ~7 coalesced
+// ones, and shrinks the per-block column from 4 to 2 bytes.
+constexpr int kTileW = 64;
+
+struct NbtView {
+  NbView nb;
+  const int* fp_off;       // ntiles + 1
+  const int* fp_node;      // footprint node ids, sorted per tile
+  const uint16_t* lcol;    // per block: index in its tile's footprint
+  const uint16_t* cpl_lcol;  // per coupling: index of m in the footprint
+  int64_t ntiles;
+  int fmax;
+};
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kBlock, (K <= 2 ? 3 : 2))
+k_nbt_spmv(NbtView T, const double2* __restrict__ x, double2* __restrict__ y,
+           const double2* __restrict__ b, KrylovCtl ctl) {
+  constexpr int G = 8;
+  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
+  constexpr int S = 4 * K + 1;  // double2 per staged node: 3K (A) + K (V) + 1 pad (banks)
+  extern __shared__ double2 sx[];
+  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  bool act[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) act[k] = (MODE == kPlain) || ctl.st[k].status == kActive;
+  const NbView& A = T.nb;
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const int64_t na = 3 * A.n_nodes;
+  double part[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+
+  for (int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
+    const int f0 = T.fp_off[t], F = T.fp_off[t + 1] - f0;
+    __syncthreads();  // previous tile's readers are done
+    for (int e = threadIdx.x; e < F * 3 * K; e += blockDim.x) {
+      const int f = e / (3 * K), c = e - f * (3 * K);
+      sx[f * S + c] = x[(int64_t)T.fp_node[f0 + f] * 3 * K + c];
+    }
+    for (int e = threadIdx.x; e < F * K; e += blockDim.x) {
+      const int f = e / K, k = e - f * K;
+      const int cfm = A.cond_fwd[T.fp_node[f0 + f]];
+      sx[f * S + 3 * K + k] = cfm >= 0 ? x[(na + cfm) * K + k] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int jb = 0; jb < kTileW; jb += kBlock / G) {
+      const int64_t i = t * kTileW + jb + threadIdx.x / G;
+      const bool valid = i < A.n_nodes;
+      double2 acc[3][K], accv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
+      int cf_i = -1;
+      if (valid) {
+        const int be = A.blk_ptr[i + 1];
+        for (int q = A.blk_ptr[i] + g; q < be; q += G) {
+          const int l = T.lcol[q];
+          double B[3][3], Im[3];
+          load_block(A, q, B, Im);
+          const double2* xm = sx + l * S;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (!act[k]) continue;
+            const double2 xs[3] = {xm[k], xm[K + k], xm[2 * K + k]};
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double2 s = acc[c][k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                s.x += B[c][d] * xs[d].x;
+                s.y += B[c][d] * xs[d].y;
+              }
+              s.x -= Im[c] * xs[c].y;
+              s.y += Im[c] * xs[c].x;
+              acc[c][k] = s;
+            }
+          }
+        }
+        cf_i = A.cond_fwd[i];
+        if (cf_i >= 0) {
+          const int ce = A.cpl_ptr[i + 1];
+          for (int q = A.cpl_ptr[i] + g; q < ce; q += G) {
+            const int l = T.cpl_lcol[q];
+            double av[3], va[3];
+            double2 Q3;
+            load_cpl(A, q, av, va, Q3);
+            const double2* xm = sx + l * S;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!act[k]) continue;
+              const double2 v = xm[3 * K + k];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                acc[c][k].x += av[c] * v.x;
+                acc[c][k].y += av[c] * v.y;
+              }
+              double2 s = accv[k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                const double2 xd = xm[d * K + k];
+                s.x += va[d] * xd.x;
+                s.y += va[d] * xd.y;
+              }
+              s.x += Q3.x * v.x - Q3.y * v.y;
+              s.y += Q3.x * v.y + Q3.y * v.x;
+              accv[k] = s;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = G / 2; o; o >>= 1) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
+            acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
+          }
+          accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
+          accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
+        }
+      }
+      if (g == 0 && valid) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (!act[k]) continue;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (c == 3 && cf_i < 0) break;
+            const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
+            const double2 v = c < 3 ? acc[c][k] : accv[k];
+            const int64_t idx = row * K + k;
+            if (MODE == kPlain) {
+              y[idx] = v;
+            } else if (MODE == kCocg) {
+              y[idx] = v;
+              const double2 pv = x[idx];
+              part[2 * k] += pv.x * v.x - pv.y * v.y;
+              part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
+            } else {
+              const double2 rv = csub(b[idx], v);
+              y[idx] = rv;
+              part[k] += rv.x * rv.x + rv.y * rv.y;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (MODE == kPlain) return;
+
+  block_sum<NV>(part, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    if (MODE == kCocg) {
+      int active = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        RhsState& s = ctl.st[k];
+        if (s.status != kActive) continue;
+        const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
+        if (pq.x == 0.0 && pq.y == 0.0) {
+          s.status = kBreakdown;
+          continue;
+        }
+        s.alpha = cdiv(s.rho, pq);
+        ++active;
+      }
+      *ctl.n_active = active;
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
+// Tile footprints: CTA per tile sorts the tile's block columns in shared
+// memory (bitonic), dedupes, and (write pass) emits the footprint and the
+// 16-bit local columns. kMaxTileCols bounds the per-tile block count.
+constexpr int kMaxTileCols = 4096;
+
+__global__ void __launch_bounds__(512)
+k_tile_footprint(const int* __restrict__ blk_ptr, const int* __restrict__ blk_col,
+                 const int* __restrict__ cpl_ptr, const int2* __restrict__ cpl_idx,
+                 int64_t n_nodes, int64_t ntiles, int write, const int* __restrict__ fp_off,
+                 int* fp_count, int* fp_node, uint16_t* lcol, uint16_t* cpl_lcol, int* bad) {
+  __shared__ int keys[kMaxTileCols];
+  __shared__ int uniq_cnt;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t i0 = t * kTileW;
+    const int64_t i1 = n_nodes < i0 + kTileW ? n_nodes : i0 + kTileW;
+    const int q0 = blk_ptr[i0], q1 = blk_ptr[i1];
+    const int C = q1 - q0;
+    if (C > kMaxTileCols) {
+      if (threadIdx.x == 0) atomicOr(bad, 1);
+      continue;
+    }
+    int P = 1;
+    while (P < C) P <<= 1;
+    __syncthreads();
+    for (int e = threadIdx.x; e < P; e += blockDim.x) keys[e] = e < C ? blk_col[q0 + e] : INT_MAX;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int e = threadIdx.x; e < P; e += blockDim.x) {
+          const int o = e ^ j;
+          if (o > e) {
+            const bool up = (e & k) == 0;
+            const int a = keys[e], bb = keys[o];
+            if ((a > bb) == up) {
+              keys[e] = bb;
+              keys[o] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // compact uniques in place (serial over P by one warp would be slow; use a
+    // two-step: mark heads, then thread 0 compacts — C is small)
+    if (threadIdx.x == 0) {
+      int u = 0;
+      for (int e = 0; e < C; ++e)
+        if (e == 0 || keys[e] != keys[e - 1]) keys[u++] = keys[e];
+      uniq_cnt = u;
+    }
+    __syncthreads();
+    const int U = uniq_cnt;
+    if (!write) {
+      if (threadIdx.x == 0) {
+        fp_count[t] = U;
+        if (U > 65535) atomicOr(bad, 1);
+      }
+      continue;
+    }
+    const int f0 = fp_off[t];
+    for (int e = threadIdx.x; e < U; e += blockDim.x) fp_node[f0 + e] = keys[e];
+    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+      const int m = blk_col[q];
+      int lo = 0, hi = U - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < m) lo = mid + 1; else hi = mid;
+      }
+      lcol[q] = (uint16_t)lo;
+    }
+    const int c0 = cpl_ptr[i0], c1 = cpl_ptr[i1];
+    for (int q = c0 + threadIdx.x; q < c1; q += blockDim.x) {
+      const int m = cpl_idx[q].x;
+      int lo = 0, hi = U - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < m) lo = mid + 1; else hi = mid;
+      }
+      cpl_lcol[q] = (uint16_t)lo;
+    }
+  }
+}
+
 // CSR (assembled, node-structured) -> NB planes. Warp per node; lane = block.
 __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __restrict__ val,
                            const int* __restrict__ nbr_off, const int* __restrict__ nbr,
                            const uint8_t* __restrict__ nbr_cond, const int* __restrict__ cond_fwd,
-                           const int* __restrict__ cpl_ptr, int64_t n_nodes, double2* blk,
-                           int64_t nblk, int2* cpl_idx, double2* cpl, int64_t ncpl, int* bad) {
+                           const int* __restrict__ cpl_ptr, int64_t n_nodes, double* blk,
+                           int64_t nblk, int2* cpl_idx, double* cpl, int64_t ncpl, int* bad) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -482,12 +821,15 @@ __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __res
           if (c == d) Im[c] = v.y; else nonzero_offdiag_im |= v.y != 0.0;
         }
       const int64_t q = nb + r;
-      blk[q] = make_double2(Bv[0][0], Bv[0][1]);
-      blk[nblk + q] = make_double2(Bv[0][2], Bv[1][0]);
-      blk[2 * nblk + q] = make_double2(Bv[1][1], Bv[1][2]);
-      blk[3 * nblk + q] = make_double2(Bv[2][0], Bv[2][1]);
-      blk[4 * nblk + q] = make_double2(Bv[2][2], Im[0]);
-      blk[5 * nblk + q] = make_double2(Im[1], Im[2]);
+      const double w0[4] = {Bv[0][0], Bv[0][1], Bv[0][2], Bv[1][0]};
+      const double w1[4] = {Bv[1][1], Bv[1][2], Bv[2][0], Bv[2][1]};
+      const double w2[4] = {Bv[2][2], Im[0], Im[1], Im[2]};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        blk[4 * q + e] = w0[e];
+        blk[4 * (nblk + q) + e] = w1[e];
+        blk[4 * (2 * nblk + q) + e] = w2[e];
+      }
       if (mc) {
         const int m = nbr[nb + r];
         const int64_t p = cb + rc;
@@ -506,10 +848,13 @@ __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __res
         }
         const double2 vv = val[basev + 3 * ncc + rc];
         cpl_idx[p] = make_int2(m, cond_fwd[m]);
-        cpl[p] = make_double2(av[0], av[1]);
-        cpl[ncpl + p] = make_double2(av[2], va[0]);
-        cpl[2 * ncpl + p] = make_double2(va[1], va[2]);
-        cpl[3 * ncpl + p] = vv;
+        const double c0[4] = {av[0], av[1], av[2], va[0]};
+        const double c1[4] = {va[1], va[2], vv.x, vv.y};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          cpl[4 * p + e] = c0[e];
+          cpl[4 * (ncpl + p) + e] = c1[e];
+        }
       }
       if (nonzero_offdiag_im) atomicOr(bad, 1);
     }
@@ -722,28 +1067,81 @@ struct Launch {
 };
 
 NbView nb_view(const ect_matrix* a) {
-  return NbView{a->nb_blk_ptr, a->nb_blk_col, a->nb_blk.p, a->nb_blocks, a->nb_cpl_ptr.p,
-                a->nb_cpl_idx.p, a->nb_cpl.p, a->nb_ncpl, a->nb_cond_fwd, a->n_nodes};
+  return NbView{a->nb_blk_ptr, a->nb_blk_col, reinterpret_cast<const double*>(a->nb_blk.p),
+                a->nb_blocks, a->nb_cpl_ptr.p, a->nb_cpl_idx.p,
+                reinterpret_cast<const double*>(a->nb_cpl.p), a->nb_ncpl, a->nb_cond_fwd,
+                a->n_nodes};
 }
 
 constexpr int kNbG = 8;  // lanes per node in the NB SpMV
+constexpr size_t kNbtMaxSmem = 110 * 1024;
+
+NbtView nbt_view(const ect_matrix* a) {
+  return NbtView{nb_view(a), a->nbt_fp_off.p, a->nbt_fp_node.p, a->nbt_lcol.p,
+                 a->nbt_cpl_lcol.p, a->nbt_tiles, a->nbt_fmax};
+}
+
+template <int K>
+size_t nbt_smem(const ect_matrix* a) {
+  return (size_t)a->nbt_fmax * (4 * K + 1) * sizeof(double2);
+}
+
+template <int K, int MODE>
+const void* nbt_fn() {
+  return (const void*)k_nbt_spmv<K, MODE>;
+}
+
+// NB kernel variant: lanes per node G and the occupancy target MINB
+// (ECT_NB_VARIANT, read at context creation; 0 is the default).
+template <int K>
+const void* nb_fn(int variant, int mode) {
+#define ECT_NBF(G_, MB_)                                                   \
+  (mode == kPlain  ? (const void*)k_nb_spmv<G_, K, kPlain, MB_>            \
+   : mode == kCocg ? (const void*)k_nb_spmv<G_, K, kCocg, MB_>             \
+                   : (const void*)k_nb_spmv<G_, K, kResid, MB_>)
+  if constexpr (K <= 2) {
+    switch (variant) {
+      case 1: return ECT_NBF(4, 1);
+      case 2: return ECT_NBF(8, 3);
+      case 3: return ECT_NBF(4, 3);
+      case 4: return ECT_NBF(8, 2);
+      case 6: return ECT_NBF(8, 1);
+      default: return ECT_NBF(4, 2);  // measured best on B200 (configs[1], k = 1, 2)
+    }
+  }
+  return ECT_NBF(8, 1);
+#undef ECT_NBF
+}
 
 template <int K>
 struct Dispatch {
   static constexpr bool kNbOk = K <= 8;
+  static constexpr bool kNbtOk = K <= 4;
+  static bool use_nbt(const ect_matrix* a) {
+    return kNbtOk && a->has_nbt && nbt_smem<K>(a) <= kNbtMaxSmem;
+  }
   static void spmv(ect_ctx* ctx, int mode, int grid, int64_t n, const ect_matrix* a,
                    const double2* x, double2* y, const double2* b, KrylovCtl ctl) {
     cudaStream_t s = ctx->stream;
+    if constexpr (kNbtOk) {
+      if (use_nbt(a)) {
+        const NbtView v = nbt_view(a);
+        const size_t sm = nbt_smem<K>(a);
+        if (mode == kPlain)
+          k_nbt_spmv<K, kPlain><<<grid, kBlock, sm, s>>>(v, x, y, b, ctl);
+        else if (mode == kCocg)
+          k_nbt_spmv<K, kCocg><<<grid, kBlock, sm, s>>>(v, x, y, b, ctl);
+        else
+          k_nbt_spmv<K, kResid><<<grid, kBlock, sm, s>>>(v, x, y, b, ctl);
+        CK_LAUNCH();
+        return;
+      }
+    }
     if constexpr (kNbOk) {
       if (a->has_nb) {
-        const NbView v = nb_view(a);
-        if (mode == kPlain)
-          k_nb_spmv<kNbG, K, kPlain><<<grid, kBlock, 0, s>>>(v, x, y, b, ctl);
-        else if (mode == kCocg)
-          k_nb_spmv<kNbG, K, kCocg><<<grid, kBlock, 0, s>>>(v, x, y, b, ctl);
-        else
-          k_nb_spmv<kNbG, K, kResid><<<grid, kBlock, 0, s>>>(v, x, y, b, ctl);
-        CK_LAUNCH();
+        NbView v = nb_view(a);
+        void* args[] = {&v, &x, &y, &b, &ctl};
+        CK(cudaLaunchKernel(nb_fn<K>(ctx->nb_variant, mode), dim3(grid), dim3(kBlock), args, 0, s));
         return;
       }
     }
@@ -772,13 +1170,18 @@ struct Dispatch {
     CK_LAUNCH();
   }
   static int spmv_grid(ect_ctx* ctx, int mode, const ect_matrix* a) {
-    if constexpr (kNbOk) {
-      if (a->has_nb) {
-        const void* f = mode == kPlain  ? (const void*)k_nb_spmv<kNbG, K, kPlain>
-                        : mode == kCocg ? (const void*)k_nb_spmv<kNbG, K, kCocg>
-                                        : (const void*)k_nb_spmv<kNbG, K, kResid>;
-        return grid_for(ctx, f, kBlock);
+    if constexpr (kNbtOk) {
+      if (use_nbt(a)) {
+        const void* f = mode == kPlain  ? nbt_fn<K, kPlain>()
+                        : mode == kCocg ? nbt_fn<K, kCocg>()
+                                        : nbt_fn<K, kResid>();
+        const size_t sm = nbt_smem<K>(a);
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        return (int)std::min<int64_t>(grid_for(ctx, f, kBlock, sm), a->nbt_tiles);
       }
+    }
+    if constexpr (kNbOk) {
+      if (a->has_nb) return grid_for(ctx, nb_fn<K>(ctx->nb_variant, mode), kBlock);
     }
     constexpr int G = K >= 4 ? 8 : 16;
     const void* f = mode == kPlain  ? (const void*)k_spmv<G, K, kPlain>
@@ -802,7 +1205,8 @@ void with_k(int k, F&& fn) {
   }
 }
 
-void prof_begin(ect_ctx* ctx, cudaEvent_t* ev) {
+// kind 0: SpMV launches, kind 1: the fused vector-update launches.
+void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0) {
   if (!ctx->prof.enabled) return;
   auto& P = ctx->prof;
   if (P.used + 2 > P.pool.size()) {
@@ -812,6 +1216,8 @@ void prof_begin(ect_ctx* ctx, cudaEvent_t* ev) {
       P.pool.push_back(e);
     }
   }
+  P.kinds.resize(P.pool.size());
+  P.kinds[P.used] = kind;
   ev[0] = P.pool[P.used++];
   ev[1] = P.pool[P.used++];
   CK(cudaEventRecord(ev[0], ctx->stream));
@@ -824,14 +1230,17 @@ void prof_collect(ect_ctx* ctx) {
   auto& P = ctx->prof;
   if (!P.enabled || P.used == 0) return;
   CK(cudaStreamSynchronize(ctx->stream));
-  double tot = 0.0;
   for (size_t i = 0; i + 1 < P.used; i += 2) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, P.pool[i], P.pool[i + 1]));
-    tot += ms;
+    if (P.kinds[i] == 0) {
+      ctx->timings.spmv_ms_total += ms;
+      ctx->timings.spmv_launches += 1;
+    } else {
+      ctx->timings.vec_ms_total += ms;
+      ctx->timings.vec_launches += 1;
+    }
   }
-  ctx->timings.spmv_ms_total += tot;
-  ctx->timings.spmv_launches += (int64_t)(P.used / 2);
   P.used = 0;
 }
 
@@ -891,7 +1300,9 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
   const int wgrid = (int)std::min<int64_t>((32 * nn + 255) / 256, (int64_t)ctx->num_sms * 16);
   k_build_nb<<<std::max(wgrid, 1), 256, 0, s>>>(a->row_ptr.p, a->val.p, m->nbr_off.p, m->nbr.p,
                                                  m->nbr_cond.p, m->cond_fwd.p, a->nb_cpl_ptr.p, nn,
-                                                 a->nb_blk.p, nblk, a->nb_cpl_idx.p, a->nb_cpl.p,
+                                                 reinterpret_cast<double*>(a->nb_blk.p), nblk,
+                                                 a->nb_cpl_idx.p,
+                                                 reinterpret_cast<double*>(a->nb_cpl.p),
                                                  ncpl, bad.p);
   CK_LAUNCH();
   note_launch(ctx, 3);
@@ -904,7 +1315,47 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
     a->nb_blk.release();
     a->nb_cpl.release();
     a->nb_cpl_idx.release();
+    return;
   }
+  // ---- NB-T tile footprints --------------------------------------------------
+  a->has_nbt = false;
+  if (ctx->no_tiles) return;
+  const int64_t ntiles = (nn + kTileW - 1) / kTileW;
+  DevBuf<int> fcnt(ntiles + 1);
+  CK(cudaMemsetAsync(fcnt.p, 0, fcnt.bytes(), s));
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  const int tgrid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 8);
+  k_tile_footprint<<<tgrid, 512, 0, s>>>(m->nbr_off.p, m->nbr.p, a->nb_cpl_ptr.p,
+                                        a->nb_cpl_idx.p, nn, ntiles, 0, nullptr, fcnt.p, nullptr,
+                                        nullptr, nullptr, bad.p);
+  CK_LAUNCH();
+  a->nbt_fp_off.alloc(ntiles + 1);
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, fcnt.p, a->nbt_fp_off.p, ntiles + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, fcnt.p, a->nbt_fp_off.p,
+                                   ntiles + 1, s));
+  int fmax = 0, ftot = 0;
+  {
+    DevBuf<int> mx(1);
+    CK(cub::DeviceReduce::Max(nullptr, tmp, fcnt.p, mx.p, ntiles, s));
+    CK(cub::DeviceReduce::Max(cub_scratch(ctx, tmp), tmp, fcnt.p, mx.p, ntiles, s));
+    CK(cudaMemcpyAsync(&fmax, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ftot, a->nbt_fp_off.p + ntiles, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  if (h_bad || fmax <= 0) return;  // too irregular for 16-bit tiles: untiled NB
+  a->nbt_fp_node.alloc(std::max(1, ftot));
+  a->nbt_lcol.alloc(std::max<int64_t>(1, nblk));
+  a->nbt_cpl_lcol.alloc(std::max(1, ncpl));
+  k_tile_footprint<<<tgrid, 512, 0, s>>>(m->nbr_off.p, m->nbr.p, a->nb_cpl_ptr.p,
+                                        a->nb_cpl_idx.p, nn, ntiles, 1, a->nbt_fp_off.p, fcnt.p,
+                                        a->nbt_fp_node.p, a->nbt_lcol.p, a->nbt_cpl_lcol.p, bad.p);
+  CK_LAUNCH();
+  note_launch(ctx, 2);
+  CK(cudaStreamSynchronize(s));
+  a->nbt_tiles = ntiles;
+  a->nbt_fmax = fmax;
+  a->has_nbt = true;
 }
 
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
@@ -991,8 +1442,11 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
           prof_begin(ctx, ev);
           DK::spmv(ctx, kCocg, grid_s, n, a, p.p, q.p, nullptr, ctl);
           prof_end(ctx, ev);
+          cudaEvent_t ev2[2];
+          prof_begin(ctx, ev2, 1);
           DK::update(ctx, grid_v, n, xx.p, r.p, p.p, q.p, a->dinv.p, ctl);
           DK::pupdate(ctx, grid_v, n, r.p, p.p, a->dinv.p, ctl);
+          prof_end(ctx, ev2);
           note_launch(ctx, 3);
         }
         launched += chunk;

@@ -80,7 +80,8 @@ class SignalPoint(C.Structure):
 
 class Timings(C.Structure):
     _fields_ = [("pattern_ms", D), ("assemble_ms", D), ("rhs_ms", D), ("solve_ms", D),
-                ("spmv_ms_total", D), ("spmv_launches", I64), ("kernel_launches", I64)]
+                ("spmv_ms_total", D), ("spmv_launches", I64), ("kernel_launches", I64),
+                ("vec_ms_total", D), ("vec_launches", I64)]
 
 
 _lib = None
@@ -148,8 +149,9 @@ class Context:
         _check(lib().ect_ctx_synchronize(self.h))
 
     def set_format(self, fmt: str):
-        """SpMV storage of matrices assembled afterwards: 'nb' (default) or 'csr'."""
-        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1}[fmt])))
+        """SpMV storage of matrices assembled afterwards: 'nb' (default),
+        'nb_tiled' (shared-memory x tiles) or 'csr'."""
+        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1, "nb_tiled": 2}[fmt])))
 
     def mark(self, slot: int):
         """Record event `slot` on the context stream (device-side timing)."""
@@ -250,7 +252,7 @@ class Matrix:
     def format(self) -> str:
         nb = I32()
         _check(lib().ect_matrix_format(self.h, C.byref(nb)))
-        return "nb" if nb.value else "csr"
+        return {0: "csr", 1: "nb", 2: "nb_tiled"}[nb.value]
 
     def export(self, values=True):
         rp = np.empty(self.n + 1, np.int32)

@@ -47,7 +47,8 @@ for fmt in formats:
         tm = ctx.timings()
         it = max(rr["iterations"] for rr in res)
         print(f"  solve k=2 profiling={prof} its={[rr['iterations'] for rr in res]} dev_ms={ms:.1f} "
-              f"ms/iter={ms / it:.4f} spmv_avg={tm['spmv_ms_total'] / max(1, tm['spmv_launches']):.4f}",
+              f"ms/iter={ms / it:.4f} spmv_avg={tm['spmv_ms_total'] / max(1, tm['spmv_launches']):.4f}"
+              f" vec_avg={tm['vec_ms_total'] / max(1, tm['vec_launches']):.4f} n_spmv={tm['spmv_launches']}",
               flush=True)
     ctx.set_profiling(False)
     del a
