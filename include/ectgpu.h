@@ -143,6 +143,8 @@ int ect_ctx_synchronize(ect_ctx* ctx);
 int ect_ctx_set_format(ect_ctx* ctx, int format);
 /* 0: CSR, 1: NB untiled, 2: NB with shared-memory x tiles. */
 int ect_matrix_format(ect_matrix* m, int32_t* nb);
+/* NB storage counts: 3x3 node blocks and conductor couplings (0 for CSR). */
+int ect_matrix_nb_counts(ect_matrix* m, int64_t* blocks, int64_t* couplings);
 /* Device-side timing on the context stream: record event `slot` (0..7), and
  * the elapsed ms between two recorded slots (waits for the later one). */
 int ect_ctx_mark(ect_ctx* ctx, int slot);

@@ -248,6 +248,13 @@ int ect_matrix_format(ect_matrix* m, int32_t* nb) {
   return guarded([&] { *nb = m->has_nb ? (m->has_nbt ? 2 : 1) : 0; });
 }
 
+int ect_matrix_nb_counts(ect_matrix* m, int64_t* blocks, int64_t* couplings) {
+  return guarded([&] {
+    *blocks = m->has_nb ? m->nb_blocks : 0;
+    *couplings = m->has_nb ? m->nb_ncpl : 0;
+  });
+}
+
 int ect_ctx_mark(ect_ctx* ctx, int slot) {
   return guarded([&] {
     require(slot >= 0 && slot < 8, ECT_ERR_OTHER, "ect_ctx_mark: slot must be in 0..7");

@@ -254,6 +254,11 @@ class Matrix:
         _check(lib().ect_matrix_format(self.h, C.byref(nb)))
         return {0: "csr", 1: "nb", 2: "nb_tiled"}[nb.value]
 
+    def nb_stats(self) -> dict:
+        b, c = I64(), I64()
+        _check(lib().ect_matrix_nb_counts(self.h, C.byref(b), C.byref(c)))
+        return {"format": self.format, "blocks": b.value, "couplings": c.value}
+
     def export(self, values=True):
         rp = np.empty(self.n + 1, np.int32)
         ci = np.empty(self.nnz, np.int32)
