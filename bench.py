@@ -297,7 +297,7 @@ def cpu_baseline_leg(a, mesh, w, positions, threads):
         zs = [positions[i % len(positions)] for i in range(nthreads)]
         b = mesh.rhs(w.coil, zs, [1] * nthreads, w.amplitude)
         bs = np.ascontiguousarray(b.T)
-        max_iter = 4
+        max_iter = 8
         out = rs.solve_iterative_batch(bs, tol=TOL, max_iter=max_iter, restart=80,
                                        threads=nthreads)
         its = int(out["iterations"].sum())
@@ -333,7 +333,7 @@ def run_reference(args):
     setup_s = time.time() - t0
     zs = [positions[i % len(positions)] for i in range(nthreads)]
     bs = np.stack([s.position_rhs(w.coil, z, 1, w.amplitude) for z in zs])
-    max_iter = 2
+    max_iter = 8  # amortises the per-call ILU(0) rebuild over a few GMRES iterations
     for _ in range(args.warmup):
         s.solve_iterative_batch(bs[:1], tol=TOL, max_iter=1, restart=80, threads=1)
     its = 0

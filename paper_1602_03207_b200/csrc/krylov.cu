@@ -363,39 +363,62 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
         m_nx = ldg_i(A.blk_col + q);
         load_block(A, q, B_nx, Im_nx);
       }
+      // (wide batches keep the accumulators for K right-hand sides instead)
+      constexpr bool kPipe = K <= 2;
       for (; q < be; q += G) {
-        const int m = m_nx;
+        int m = m_nx;
         double B[3][3], Im[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          Im[c] = Im_nx[c];
-#pragma unroll
-          for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
-        }
-        if (q + G < be) {
-          m_nx = ldg_i(A.blk_col + q + G);
-          load_block(A, q + G, B_nx, Im_nx);
-        }
-        const double2* xm = x + (int64_t)3 * m * K;
-        double2 xk[3][K];
-        load_xk<K>(xm, xk[0]);
-        load_xk<K>(xm + K, xk[1]);
-        load_xk<K>(xm + 2 * K, xk[2]);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if (!act[k]) continue;
-          const double2 xs[3] = {xk[0][k], xk[1][k], xk[2][k]};
+        if constexpr (kPipe) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            double2 s = acc[c][k];
+            Im[c] = Im_nx[c];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              s.x += B[c][d] * xs[d].x;
-              s.y += B[c][d] * xs[d].y;
+            for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
+          }
+          if (q + G < be) {
+            m_nx = ldg_i(A.blk_col + q + G);
+            load_block(A, q + G, B_nx, Im_nx);
+          }
+        } else {
+          if (q != A.blk_ptr[i] + g) {
+            m = ldg_i(A.blk_col + q);
+            load_block(A, q, B, Im);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              Im[c] = Im_nx[c];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
             }
-            s.x -= Im[c] * xs[c].y;
-            s.y += Im[c] * xs[c].x;
-            acc[c][k] = s;
+          }
+        }
+        const double2* xm = x + (int64_t)3 * m * K;
+        // right-hand sides in pairs: one 256-bit gather per (component, pair)
+        constexpr int KP = (K % 2 == 0) ? 2 : 1;
+#pragma unroll
+        for (int k0 = 0; k0 < K; k0 += KP) {
+          if (!act[k0] && !act[k0 + KP - 1]) continue;
+          double2 xp[3][KP];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if constexpr (KP == 2) ld4x(xm + d * K + k0, xp[d][0], xp[d][1]);
+            else xp[d][0] = __ldg(xm + d * K + k0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) {
+            const int k = k0 + kk;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double2 s = acc[c][k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                s.x += B[c][d] * xp[d][kk].x;
+                s.y += B[c][d] * xp[d][kk].y;
+              }
+              s.x -= Im[c] * xp[c][kk].y;
+              s.y += Im[c] * xp[c][kk].x;
+              acc[c][k] = s;
+            }
           }
         }
       }
@@ -408,27 +431,40 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           double2 Q3;
           load_cpl(A, q, av, va, Q3);
           const double2* xm = x + (int64_t)3 * mi.x * K;
-          double2 xvk[K];
-          load_xk<K>(x + (na + mi.y) * K, xvk);
+          const double2* xvp = x + (na + mi.y) * K;
+          constexpr int KP = (K % 2 == 0) ? 2 : 1;
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (!act[k]) continue;
-            const double2 v = xvk[k];
+          for (int k0 = 0; k0 < K; k0 += KP) {
+            if (!act[k0] && !act[k0 + KP - 1]) continue;
+            double2 xa[3][KP], xv[KP];
+            if constexpr (KP == 2) {
+              ld4x(xvp + k0, xv[0], xv[1]);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              acc[c][k].x += av[c] * v.x;
-              acc[c][k].y += av[c] * v.y;
+              for (int d = 0; d < 3; ++d) ld4x(xm + d * K + k0, xa[d][0], xa[d][1]);
+            } else {
+              xv[0] = __ldg(xvp + k0);
+#pragma unroll
+              for (int d = 0; d < 3; ++d) xa[d][0] = __ldg(xm + d * K + k0);
             }
-            double2 s = accv[k];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const double2 xd = xm[d * K + k];
-              s.x += va[d] * xd.x;
-              s.y += va[d] * xd.y;
+            for (int kk = 0; kk < KP; ++kk) {
+              const int k = k0 + kk;
+              const double2 v = xv[kk];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                acc[c][k].x += av[c] * v.x;
+                acc[c][k].y += av[c] * v.y;
+              }
+              double2 s = accv[k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                s.x += va[d] * xa[d][kk].x;
+                s.y += va[d] * xa[d][kk].y;
+              }
+              s.x += Q3.x * v.x - Q3.y * v.y;
+              s.y += Q3.x * v.y + Q3.y * v.x;
+              accv[k] = s;
             }
-            s.x += Q3.x * v.x - Q3.y * v.y;
-            s.y += Q3.x * v.y + Q3.y * v.x;
-            accv[k] = s;
           }
         }
       }
@@ -1099,7 +1135,7 @@ const void* nb_fn(int variant, int mode) {
   (mode == kPlain  ? (const void*)k_nb_spmv<G_, K, kPlain, MB_>            \
    : mode == kCocg ? (const void*)k_nb_spmv<G_, K, kCocg, MB_>             \
                    : (const void*)k_nb_spmv<G_, K, kResid, MB_>)
-  if constexpr (K <= 2) {
+  if constexpr (K <= 4) {
     switch (variant) {
       case 1: return ECT_NBF(4, 1);
       case 2: return ECT_NBF(8, 3);
