@@ -563,10 +563,10 @@ struct NbtView {
 };
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(kBlock, (K <= 2 ? 3 : 2))
+__global__ void __launch_bounds__(kBlock, 2)
 k_nbt_spmv(NbtView T, const double2* __restrict__ x, double2* __restrict__ y,
            const double2* __restrict__ b, KrylovCtl ctl) {
-  constexpr int G = 8;
+  constexpr int G = 4;
   constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
   constexpr int S = 4 * K + 1;  // double2 per staged node: 3K (A) + K (V) + 1 pad (banks)
   extern __shared__ double2 sx[];
@@ -605,10 +605,26 @@ k_nbt_spmv(NbtView T, const double2* __restrict__ x, double2* __restrict__ y,
       int cf_i = -1;
       if (valid) {
         const int be = A.blk_ptr[i + 1];
-        for (int q = A.blk_ptr[i] + g; q < be; q += G) {
-          const int l = T.lcol[q];
+        int q = A.blk_ptr[i] + g;
+        int l_nx = 0;
+        double B_nx[3][3], Im_nx[3];
+        if (q < be) {
+          l_nx = T.lcol[q];
+          load_block(A, q, B_nx, Im_nx);
+        }
+        for (; q < be; q += G) {
+          const int l = l_nx;
           double B[3][3], Im[3];
-          load_block(A, q, B, Im);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            Im[c] = Im_nx[c];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
+          }
+          if (q + G < be) {
+            l_nx = T.lcol[q + G];
+            load_block(A, q + G, B_nx, Im_nx);
+          }
           const double2* xm = sx + l * S;
 #pragma unroll
           for (int k = 0; k < K; ++k) {
