@@ -75,6 +75,8 @@ typedef struct ect_physics {
   double bc_penalty;
   int32_t mu_tilde_harmonic;
   double mu_tilde_fixed;
+  double sigma_tsp;  /* < 0: default 5e6 (config.hpp:29) */
+  double mu_r_tsp;   /* < 0: default 50 (config.hpp:30) */
 } ect_physics;
 
 /* CoilPair (tube_mesh.hpp:13-21). */

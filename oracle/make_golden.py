@@ -147,6 +147,34 @@ def make_cfg1():
     (GOLDEN / "cfg1.json").write_text(json.dumps(out, indent=1))
 
 
+TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
+
+
+def make_trace():
+    """5-position sweep on small_6x6x12 through the reference (direct LU per
+    material configuration, delta_impedance x4, signal_modes) written by the
+    reference's write_trace_csv (scan.cpp:170-207)."""
+    w = workloads.small(**SMALL_CASES["small_6x6x12"])
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    assert two
+    sp = ref.RefSystem(rm, prim)
+    sr = ref.RefSystem(rm, refm)
+    b = np.stack([sp.position_rhs(w.coil, z, c, w.amplitude) for z in TRACE_Z for c in (1, 2)])
+    xp, _ = sp.solve_direct(b)
+    xr, _ = sr.solve_direct(b)
+    dzs, modes = [], []
+    for i in range(len(TRACE_Z)):
+        dz = np.array([rm.delta_impedance(prim, refm, xp[2 * i + k], xr[2 * i + l])
+                       for k in range(2) for l in range(2)])
+        dzs.append(dz)
+        modes.append(ref.signal_modes(dz))
+    ref.trace_write(GOLDEN / "trace_small_6x6x12.csv", np.array(TRACE_Z), np.array(dzs),
+                    np.array(modes), config_hash="small_6x6x12")
+    print("trace written", GOLDEN / "trace_small_6x6x12.csv")
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what in ("small", "all"):
@@ -155,3 +183,5 @@ if __name__ == "__main__":
         make_cfg0()
     if what in ("cfg1", "all"):
         make_cfg1()
+    if what in ("trace", "all"):
+        make_trace()

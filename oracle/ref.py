@@ -38,7 +38,8 @@ class Physics(C.Structure):
                 ("sigma_defect", C.c_double), ("mu_r_defect", C.c_double),
                 ("sigma_eps_ratio", C.c_double), ("delta_gauge", C.c_double),
                 ("bc_penalty", C.c_double), ("mu_tilde_harmonic", C.c_int32),
-                ("mu_tilde_fixed", C.c_double)]
+                ("mu_tilde_fixed", C.c_double), ("sigma_tsp", C.c_double),
+                ("mu_r_tsp", C.c_double)]
 
 
 def build_if_possible() -> bool:
@@ -87,7 +88,7 @@ I64 = C.c_int64
 def physics_struct(ph) -> Physics:
     return Physics(ph.frequency, ph.sigma_tube, ph.mu_r_tube, ph.sigma_defect, ph.mu_r_defect,
                    ph.sigma_eps_ratio, ph.delta_gauge, ph.bc_penalty, int(ph.mu_tilde_harmonic),
-                   ph.mu_tilde_fixed)
+                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp)
 
 
 class RefMesh:
@@ -260,3 +261,19 @@ def system_from_csc(col_ptr, row_idx, values) -> "RefSystem":
     s.h, s.mesh, s.timings = h, None, {}
     s.n, s.nnz, s.n_pins = len(col_ptr) - 1, len(row_idx), 0
     return s
+
+
+def trace_write(path, z, dz, modes, failed=None, config_hash=""):
+    """The reference's write_trace_csv (scan.cpp:170-207)."""
+    z = np.ascontiguousarray(z, np.float64)
+    dz = np.ascontiguousarray(np.asarray(dz, np.complex128).reshape(len(z), 4))
+    modes = np.ascontiguousarray(np.asarray(modes, np.complex128).reshape(len(z), 2))
+    f = np.ascontiguousarray(np.zeros(len(z)) if failed is None else failed, np.int32)
+    _check(lib().ref_trace_write(str(path).encode(), I32(len(z)), _p(z, D), _p(dz, D),
+                                 _p(modes, D), _p(f, I32), config_hash.encode()))
+
+
+def trace_max_relative_deviation(a, b):
+    out = D()
+    _check(lib().ref_trace_max_relative_deviation(str(a).encode(), str(b).encode(), C.byref(out)))
+    return out.value

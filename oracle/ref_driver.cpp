@@ -33,6 +33,7 @@
 #include "ectsim/materials.hpp"
 #include "ectsim/mesh.hpp"
 #include "ectsim/partition.hpp"
+#include "ectsim/scan.hpp"
 #include "ectsim/signals.hpp"
 #include "ectsim/solver.hpp"
 #include "ectsim/sparse.hpp"
@@ -111,6 +112,8 @@ struct ref_physics {
   double bc_penalty;
   int32_t mu_tilde_harmonic;
   double mu_tilde_fixed;
+  double sigma_tsp;  // < 0: default (config.hpp:29)
+  double mu_r_tsp;   // < 0: default (config.hpp:30)
 };
 
 static MaterialTable unpack(const ref_materials* m) {
@@ -226,6 +229,8 @@ int ref_materials_from_physics(void* h, const ref_physics* p, ref_materials* pri
     cfg.bc_penalty = p->bc_penalty;
     cfg.mu_tilde_policy = p->mu_tilde_harmonic ? "harmonic" : "fixed";
     cfg.mu_tilde_fixed = p->mu_tilde_fixed;
+    if (p->sigma_tsp >= 0) cfg.sigma_tsp = p->sigma_tsp;
+    if (p->mu_r_tsp >= 0) cfg.mu_r_tsp = p->mu_r_tsp;
     MaterialTable mats = cfg.material_table();
     cfg.resolve_mu_tilde(mats, m->mesh);
     MaterialTable ref = reference_variant(mats);
@@ -454,6 +459,31 @@ void ref_signal_modes(const double* dz, double* out) {
   out[1] = s.z_fa.imag();
   out[2] = s.z_f3.real();
   out[3] = s.z_f3.imag();
+}
+
+// write_trace_csv (scan.cpp:170-207) of n points: dz = 8 doubles per point,
+// modes = 4 doubles per point (z_fa, z_f3).
+int ref_trace_write(const char* path, int32_t n, const double* z, const double* dz,
+                    const double* modes, const int32_t* failed, const char* config_hash) {
+  return guarded([&] {
+    ImpedanceTrace tr;
+    tr.config_hash = config_hash ? config_hash : "";
+    for (int i = 0; i < n; ++i) {
+      SignalPoint p;
+      p.z = z[i];
+      for (int q = 0; q < 4; ++q) p.delta_z.z[q / 2][q % 2] = complexd(dz[8 * i + 2 * q], dz[8 * i + 2 * q + 1]);
+      p.z_fa = complexd(modes[4 * i], modes[4 * i + 1]);
+      p.z_f3 = complexd(modes[4 * i + 2], modes[4 * i + 3]);
+      p.failed = failed && failed[i];
+      tr.points.push_back(p);
+    }
+    write_trace_csv(tr, path);
+  });
+}
+
+// read_trace_csv x2 + max_relative_deviation (scan.cpp:209-272).
+int ref_trace_max_relative_deviation(const char* a, const char* b, double* out) {
+  return guarded([&] { *out = max_relative_deviation(read_trace_csv(a), read_trace_csv(b)); });
 }
 
 // Element forms for known-answer checks (element_forms.cpp:8-114).

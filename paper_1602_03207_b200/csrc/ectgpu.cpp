@@ -418,7 +418,8 @@ int ect_materials_from_physics(ect_mesh* mesh, const ect_physics* ph, ect_materi
       m.mu[r] = mu;
     };
     set(ECT_REGION_TUBE, ph->sigma_tube, kMu0 * ph->mu_r_tube);
-    set(ECT_REGION_TSP, 5e6, kMu0 * 50.0);
+    set(ECT_REGION_TSP, ph->sigma_tsp >= 0 ? ph->sigma_tsp : 5e6,
+        kMu0 * (ph->mu_r_tsp >= 0 ? ph->mu_r_tsp : 50.0));
     set(ECT_REGION_DEFECT, ph->sigma_defect >= 0 ? ph->sigma_defect : ph->sigma_tube,
         kMu0 * (ph->mu_r_defect >= 0 ? ph->mu_r_defect : ph->mu_r_tube));
     set(ECT_REGION_COIL1, 0.0, kMu0);

@@ -58,7 +58,8 @@ class Materials(C.Structure):
 class Physics(C.Structure):
     _fields_ = [("frequency", D), ("sigma_tube", D), ("mu_r_tube", D), ("sigma_defect", D),
                 ("mu_r_defect", D), ("sigma_eps_ratio", D), ("delta_gauge", D),
-                ("bc_penalty", D), ("mu_tilde_harmonic", I32), ("mu_tilde_fixed", D)]
+                ("bc_penalty", D), ("mu_tilde_harmonic", I32), ("mu_tilde_fixed", D),
+                ("sigma_tsp", D), ("mu_r_tsp", D)]
 
 
 class Coil(C.Structure):
@@ -116,7 +117,7 @@ def _ptr(a):
 def physics_struct(ph) -> Physics:
     return Physics(ph.frequency, ph.sigma_tube, ph.mu_r_tube, ph.sigma_defect, ph.mu_r_defect,
                    ph.sigma_eps_ratio, ph.delta_gauge, ph.bc_penalty, int(ph.mu_tilde_harmonic),
-                   ph.mu_tilde_fixed)
+                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp)
 
 
 class Context:

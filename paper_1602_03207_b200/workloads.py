@@ -40,6 +40,8 @@ class Physics:
     bc_penalty: float = 1e13
     mu_tilde_harmonic: bool = True
     mu_tilde_fixed: float = 1.25663706212e-6
+    sigma_tsp: float = -1.0      # <0: default (config.hpp:29)
+    mu_r_tsp: float = -1.0
 
 
 @dataclass
