@@ -79,7 +79,7 @@ def centroids(xyz: np.ndarray, tets: np.ndarray) -> np.ndarray:
 
 def kuhn_box(nx: int, ny: int, nz: int, *, extent=(1.0, 1.0, 2.0), seed: int | None = 0,
              jitter: float = 0.1, origin=(0.2, 0.5), scale: float = 0.01,
-             slab=(0.4, 0.6), deposits=((0.9, 1.1),)) -> BoxMesh:
+             slab=(0.4, 0.6), deposits=((0.9, 1.1),), tsp_deposits=()) -> BoxMesh:
     """Jittered Kuhn box; see module docstring for the conventions."""
     lx, ly, lz = extent
     hx, hy, hz = lx / nx, ly / ny, lz / nz
@@ -126,6 +126,11 @@ def kuhn_box(nx: int, ny: int, nz: int, *, extent=(1.0, 1.0, 2.0), seed: int | N
     region[in_slab] = TUBE
     for z0, z1 in deposits:
         region[in_slab & (c[:, 2] >= z0) & (c[:, 2] <= z1)] = DEFECT
+    # further deposits with their own (sigma, mu): the reference's MaterialTable
+    # holds one pair per RegionTag, so they take the TSP tag (a conductor region,
+    # types.hpp:46-48, excluded from dZ which integrates DEFECT only)
+    for z0, z1 in tsp_deposits:
+        region[in_slab & (c[:, 2] >= z0) & (c[:, 2] <= z1)] = TSP
 
     xyz_m = np.empty_like(xyz)
     xyz_m[:, 0] = (xyz[:, 0] - origin[0]) * scale

@@ -814,7 +814,7 @@ k_tile_footprint(const int* __restrict__ blk_ptr, const int* __restrict__ blk_co
       const int m = blk_col[q];
       int lo = 0, hi = U - 1;
       while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1);
         if (keys[mid] < m) lo = mid + 1; else hi = mid;
       }
       lcol[q] = (uint16_t)lo;
@@ -824,7 +824,7 @@ k_tile_footprint(const int* __restrict__ blk_ptr, const int* __restrict__ blk_co
       const int m = cpl_idx[q].x;
       int lo = 0, hi = U - 1;
       while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1);
         if (keys[mid] < m) lo = mid + 1; else hi = mid;
       }
       cpl_lcol[q] = (uint16_t)lo;
@@ -1099,7 +1099,7 @@ __global__ void k_jacobi(int64_t n, const int* __restrict__ row_ptr, const int* 
     int lo = row_ptr[i], hi = row_ptr[i + 1] - 1;
     int pos = -1;
     while (lo <= hi) {
-      int mid = (lo + hi) >> 1;
+      int mid = lo + ((hi - lo) >> 1);  // no int overflow at nnz > 2^30
       int c = col[mid];
       if (c == i) { pos = mid; break; }
       if (c < i) lo = mid + 1; else hi = mid - 1;

@@ -176,7 +176,7 @@ __global__ void k_csr_to_csc(const int* __restrict__ row_ptr, const int* __restr
       const int j = col[p];
       int lo = row_ptr[j], hi = row_ptr[j + 1] - 1;
       while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1);
         if (col[mid] < (int)i) lo = mid + 1; else hi = mid;
       }
       out[lo] = val[p];

@@ -61,7 +61,8 @@ class Workload:
 
     def mesh(self) -> BoxMesh:
         return kuhn_box(*self.dims, extent=self.extent, seed=self.seed, origin=COIL_AXIS,
-                        scale=SCALE, deposits=self.deposits)
+                        scale=SCALE, deposits=self.deposits,
+                        tsp_deposits=self.extra.get("tsp_deposits", ()))
 
 
 def _coil(nz: int, lz: float = 2.0) -> tuple:
@@ -94,6 +95,17 @@ def config3() -> Workload:
     return w
 
 
+def config4() -> Workload:
+    """configs[4]: 128x128x512 cells (50.3M tets) on a [0,1]x[0,1]x[0,4] box so
+    that h_z = h_x and the second deposit z in [2.5, 2.7] lies inside (SURVEY
+    §8(d)); second deposit sigma = 5e3, mu_r = 2 via the TSP tag."""
+    return Workload("configs[4]", (128, 128, 512), 3, ((0.9, 1.1),),
+                    Physics(sigma_defect=1e4, mu_r_defect=5.0, sigma_tsp=5e3, mu_r_tsp=2.0),
+                    _coil(512, 4.0), 1e6, (1.0 * SCALE,), extent=(1.0, 1.0, 4.0),
+                    notes="large mesh (single-GPU run; the z-slab split is round 2)",
+                    extra={"tsp_deposits": ((2.5, 2.7),)})
+
+
 def small(n=(4, 4, 8), seed=7, deposit=True) -> Workload:
     """Small configs[1]-like case for golden fixtures and fast tests."""
     nx, ny, nz = n
@@ -103,4 +115,5 @@ def small(n=(4, 4, 8), seed=7, deposit=True) -> Workload:
                     (1.0 * SCALE,))
 
 
-BY_NAME = {"configs[0]": config0, "configs[1]": config1, "configs[3]": config3}
+BY_NAME = {"configs[0]": config0, "configs[1]": config1, "configs[3]": config3,
+           "configs[4]": config4}
