@@ -242,6 +242,47 @@ int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
                                 int32_t positions_per_batch, ect_signal_point* out,
                                 double* solutions);
 
+/* ---- distributed solve: row partition over GPUs (SURVEY §8(e), configs[4]) --
+ * A part owns a contiguous node range [splits[part], splits[part+1]) — with
+ * the reference node numbering a slab of i-planes — i.e. its A-rows and the
+ * V-rows of its conductor nodes. Per SpMV the ghost values are exchanged with
+ * the neighbour parts (NCCL send/recv over NVLink) and each iteration's dot
+ * products are summed across parts (ncclAllReduce of <= 4 n_rhs doubles).
+ * Replaces nothing in the reference (its solve is serial); the paper's
+ * mpiAllReduce of matrices is the closest analogue. */
+typedef struct ect_halo_plan ect_halo_plan;
+typedef struct ect_part ect_part;
+typedef struct ect_comm ect_comm;
+/* Host-only halo plan from the node neighbour lists (no GPU needed).
+ * info: n0, n1, L (owned nodes), G (ghost nodes), c0 (first owned V-dof),
+ * Vo, Vg (owned / ghost V-dofs), n_peers. */
+int ect_halo_plan_create(int64_t n_nodes, const int32_t* nbr_off, const int32_t* nbr,
+                         const int32_t* cond_fwd, const int64_t* splits, int32_t n_parts,
+                         int32_t part, ect_halo_plan** out);
+int ect_halo_plan_destroy(ect_halo_plan* p);
+int ect_halo_plan_info(ect_halo_plan* p, int64_t info[8]);
+int ect_halo_plan_arrays(ect_halo_plan* p, int32_t* ghost_nodes, int32_t* local_vdof);
+/* peer info: part, recv_node_begin, recv_node_count, recv_v_begin, recv_v_count,
+ * n_send_nodes, n_send_cond_nodes (+ the send lists, local node ids). */
+int ect_halo_plan_peer(ect_halo_plan* p, int32_t i, int64_t info[7], int32_t* send_nodes,
+                       int32_t* send_cond_nodes);
+/* NCCL communicator (libnccl.so.2 loaded at run time). */
+int ect_comm_unique_id(void* out128);
+int ect_comm_create(ect_ctx* ctx, int32_t rank, int32_t world, const void* id128, ect_comm** out);
+int ect_comm_destroy(ect_comm* c);
+/* One part of an assembled (NB) global matrix on ctx's GPU. info: n0, n1, L,
+ * G, Vo, Vg, n_peers, n_blocks. */
+int ect_part_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix* m, const int64_t* splits,
+                    int32_t n_parts, int32_t part, ect_part** out);
+int ect_part_destroy(ect_part* p);
+int ect_part_info(ect_part* p, int64_t info[8]);
+/* Partitioned Jacobi-COCG on GLOBAL b/x ([n][n_rhs]); each part reads and
+ * writes its owned rows. comm == NULL: all n_parts parts live in this
+ * process on one context (halo = device copies); else n_parts == 1 and the
+ * halo / reductions go through NCCL. */
+int ect_dist_solve(ect_part** parts, int32_t n_parts, ect_comm* comm, const double* b, double* x,
+                   int32_t n_rhs, const ect_iter_options* opts, ect_iter_result* results);
+
 #ifdef __cplusplus
 }
 #endif

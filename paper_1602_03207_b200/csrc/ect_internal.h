@@ -160,6 +160,31 @@ struct ect_matrix {
   ect::DevBuf<uint16_t> nbt_lcol, nbt_cpl_lcol;
 };
 
+#include "dist_plan.h"
+
+// One row partition of the global matrix on one GPU (distributed solve).
+struct ect_part {
+  ect_ctx* ctx = nullptr;
+  ect::HaloPlan plan;
+  int64_t n_global = 0, na_global = 0, n_nodes_global = 0;
+  int64_t nblk = 0, ncpl = 0;
+  ect::DevBuf<int> blk_ptr, blk_col, cpl_ptr, cond_local;
+  ect::DevBuf<int2> cpl_idx;
+  ect::DevBuf<double2> blk, cpl, dinv;  // NB planes (3 x 4 doubles, 2 x 4 doubles), local dinv
+  struct Peer {
+    ect::DevBuf<int> send_nodes, send_cond;
+    ect::DevBuf<double2> sendbuf;
+    int64_t ns = 0, nsc = 0;
+  };
+  std::vector<Peer> peers;  // parallel to plan.peers
+};
+
+// NCCL communicator for the distributed solve (loaded with dlopen).
+struct ect_comm {
+  int rank = 0, world = 1;
+  void* comm = nullptr;  // ncclComm_t
+};
+
 namespace ect {
 
 // Buffer argument that may be host or device memory.
@@ -185,6 +210,19 @@ struct SolveOut {
 };
 void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
                 const ect_iter_options& opt, SolveOut* out);  // krylov.cu
+
+// distributed solve (krylov.cu)
+ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_parts, int part);
+void dist_solve(ect_part** parts, int n_parts, ect_comm* comm, const double2* b_global,
+                double2* x_global, int k, const ect_iter_options& opt, SolveOut* out);
+// NCCL entry points resolved at runtime (ectgpu.cpp)
+struct NcclApi;
+const NcclApi* nccl_api();
+void nccl_allreduce_sum(ect_comm* c, double* buf, size_t n, cudaStream_t s);
+void nccl_group_start();
+void nccl_group_end();
+void nccl_send(ect_comm* c, const void* buf, size_t n_doubles, int peer, cudaStream_t s);
+void nccl_recv(ect_comm* c, void* buf, size_t n_doubles, int peer, cudaStream_t s);
 
 // cub temporary storage helper
 void* cub_scratch(ect_ctx* ctx, size_t bytes);

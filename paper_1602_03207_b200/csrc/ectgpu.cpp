@@ -777,3 +777,216 @@ int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
 }
 
 }  // extern "C"
+
+// ============================================================================
+// Distributed solve: halo plans (host only), parts, NCCL transport.
+#include <dlfcn.h>
+#include <nccl.h>
+
+struct ect_halo_plan {
+  ect::HaloPlan plan;
+};
+
+namespace ect {
+
+struct NcclApi {
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+// NCCL is resolved at run time (dlopen of libnccl.so.2, which reuses the copy
+// torch.distributed already loaded), so libectgpu.so has no link dependency.
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool loaded = [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+    api.send = reinterpret_cast<decltype(api.send)>(dlsym(h, "ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(h, "ncclRecv"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(h, "ncclGetErrorString"));
+    return api.getUniqueId && api.commInitRank && api.allReduce && api.send && api.recv &&
+           api.groupStart && api.groupEnd;
+  }();
+  if (!loaded) fail(ECT_ERR_CUDA, "NCCL (libnccl.so.2) could not be loaded");
+  return &api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    const NcclApi* a = nccl_api();
+    fail(ECT_ERR_CUDA, std::string(what) + ": " + (a->errorString ? a->errorString(r) : "nccl error"));
+  }
+}
+
+void nccl_allreduce_sum(ect_comm* c, double* buf, size_t n, cudaStream_t s) {
+  nccl_check(nccl_api()->allReduce(buf, buf, n, ncclFloat64, ncclSum,
+                                   static_cast<ncclComm_t>(c->comm), s), "ncclAllReduce");
+}
+void nccl_group_start() { nccl_check(nccl_api()->groupStart(), "ncclGroupStart"); }
+void nccl_group_end() { nccl_check(nccl_api()->groupEnd(), "ncclGroupEnd"); }
+void nccl_send(ect_comm* c, const void* buf, size_t n_doubles, int peer, cudaStream_t s) {
+  nccl_check(nccl_api()->send(buf, n_doubles, ncclFloat64, peer, static_cast<ncclComm_t>(c->comm), s),
+             "ncclSend");
+}
+void nccl_recv(ect_comm* c, void* buf, size_t n_doubles, int peer, cudaStream_t s) {
+  nccl_check(nccl_api()->recv(buf, n_doubles, ncclFloat64, peer, static_cast<ncclComm_t>(c->comm), s),
+             "ncclRecv");
+}
+
+}  // namespace ect
+
+extern "C" {
+
+int ect_halo_plan_create(int64_t n_nodes, const int32_t* nbr_off, const int32_t* nbr,
+                         const int32_t* cond_fwd, const int64_t* splits, int32_t n_parts,
+                         int32_t part, ect_halo_plan** out) {
+  return guarded([&] {
+    auto p = std::make_unique<ect_halo_plan>();
+    try {
+      p->plan = ect::build_halo_plan(n_nodes, nbr_off, nbr, cond_fwd, splits, n_parts, part);
+    } catch (const std::invalid_argument& e) {
+      ect::fail(ECT_ERR_CONFIG, e.what());
+    }
+    *out = p.release();
+  });
+}
+
+int ect_halo_plan_destroy(ect_halo_plan* p) {
+  return guarded([&] { delete p; });
+}
+
+int ect_halo_plan_info(ect_halo_plan* p, int64_t info[8]) {
+  return guarded([&] {
+    const auto& H = p->plan;
+    const int64_t v[8] = {H.n0, H.n1, H.L, H.G, H.c0, H.Vo, H.Vg, (int64_t)H.peers.size()};
+    for (int i = 0; i < 8; ++i) info[i] = v[i];
+  });
+}
+
+int ect_halo_plan_arrays(ect_halo_plan* p, int32_t* ghost_nodes, int32_t* local_vdof) {
+  return guarded([&] {
+    const auto& H = p->plan;
+    if (ghost_nodes) std::memcpy(ghost_nodes, H.ghost_nodes.data(), H.G * sizeof(int32_t));
+    if (local_vdof) std::memcpy(local_vdof, H.local_vdof.data(), (H.L + H.G) * sizeof(int32_t));
+  });
+}
+
+int ect_halo_plan_peer(ect_halo_plan* p, int32_t i, int64_t info[7], int32_t* send_nodes,
+                       int32_t* send_cond_nodes) {
+  return guarded([&] {
+    const auto& H = p->plan;
+    require(i >= 0 && i < (int)H.peers.size(), ECT_ERR_CONFIG, "halo plan: peer index out of range");
+    const auto& q = H.peers[i];
+    const int64_t v[7] = {q.part, q.recv_node_begin, q.recv_node_count, q.recv_v_begin,
+                          q.recv_v_count, (int64_t)q.send_nodes.size(),
+                          (int64_t)q.send_cond_nodes.size()};
+    for (int j = 0; j < 7; ++j) info[j] = v[j];
+    if (send_nodes) std::memcpy(send_nodes, q.send_nodes.data(), q.send_nodes.size() * 4);
+    if (send_cond_nodes)
+      std::memcpy(send_cond_nodes, q.send_cond_nodes.data(), q.send_cond_nodes.size() * 4);
+  });
+}
+
+int ect_comm_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    ect::nccl_check(ect::nccl_api()->getUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int ect_comm_create(ect_ctx* ctx, int32_t rank, int32_t world, const void* id128, ect_comm** out) {
+  return guarded([&] {
+    ScopedDevice sd(ctx->device);
+    auto c = std::make_unique<ect_comm>();
+    c->rank = rank;
+    c->world = world;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm = nullptr;
+    ect::nccl_check(ect::nccl_api()->commInitRank(&comm, world, id, rank), "ncclCommInitRank");
+    c->comm = comm;
+    *out = c.release();
+  });
+}
+
+int ect_comm_destroy(ect_comm* c) {
+  return guarded([&] {
+    if (!c) return;
+    if (c->comm) ect::nccl_api()->commDestroy(static_cast<ncclComm_t>(c->comm));
+    delete c;
+  });
+}
+
+int ect_part_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix* a, const int64_t* splits,
+                    int32_t n_parts, int32_t part, ect_part** out) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(a->assembled, ECT_ERR_SOLVER, "part: matrix values not assembled");
+    try {
+      *out = ect::create_part(mesh, a, splits, n_parts, part);
+    } catch (const std::invalid_argument& e) {
+      ect::fail(ECT_ERR_CONFIG, e.what());
+    }
+  });
+}
+
+int ect_part_destroy(ect_part* p) {
+  return guarded([&] {
+    if (!p) return;
+    ScopedDevice sd(p->ctx->device);
+    delete p;
+  });
+}
+
+int ect_part_info(ect_part* p, int64_t info[8]) {
+  return guarded([&] {
+    const auto& H = p->plan;
+    const int64_t v[8] = {H.n0, H.n1, H.L, H.G, H.Vo, H.Vg, (int64_t)H.peers.size(), p->nblk};
+    for (int i = 0; i < 8; ++i) info[i] = v[i];
+  });
+}
+
+int ect_dist_solve(ect_part** parts, int32_t n_parts, ect_comm* comm, const double* b, double* x,
+                   int32_t n_rhs, const ect_iter_options* opts, ect_iter_result* results) {
+  return guarded([&] {
+    require(n_parts >= 1 && parts && parts[0], ECT_ERR_SOLVER, "dist_solve: no parts");
+    ect_ctx* ctx = parts[0]->ctx;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    ect_iter_options o = opts ? *opts : ect_iter_options{1e-8, 500, 80};
+    const size_t cnt = (size_t)parts[0]->n_global * n_rhs;
+    In<double2> bi(ctx, reinterpret_cast<const double2*>(b), cnt);
+    // x is written only on the rows the given parts own: stage the caller's
+    // buffer so untouched rows keep their values
+    Out<double2> xo(ctx, reinterpret_cast<double2*>(x), cnt);
+    if (xo.host) CK(cudaMemcpyAsync(xo.dev, x, cnt * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    ect::SolveOut so;
+    {
+      EventTimer t(ctx, &ctx->timings.solve_ms);
+      ect::dist_solve(parts, n_parts, comm, bi.dev, xo.dev, n_rhs, o, &so);
+    }
+    xo.finish();
+    for (int c = 0; c < n_rhs; ++c) {
+      results[c].iterations = so.iters[c];
+      results[c].residual = so.residual[c];
+      results[c].converged = so.converged[c];
+    }
+  });
+}
+
+}  // extern "C"

@@ -124,7 +124,109 @@ struct KrylovCtl {
   double* partial;    // [grid][NV]
   double tol;
   int max_iter;
+  // distributed solve: the last block writes its (part-local) totals here and
+  // the finalisation runs after the cross-part reduction (k_fin); nullptr on
+  // a single part, where the last block finalises directly
+  double* red;
+  // owned rows of the vector kernels: [s0, e0) U [s1, e1)
+  int64_t s0, e0, s1, e1;
 };
+
+// ---- scalar finalisations (run by one thread on the global totals) ----------
+template <int K>
+__device__ void fin_alpha(const KrylovCtl& ctl, const double* tot) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    if (s.status != kActive) continue;
+    const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
+    if (pq.x == 0.0 && pq.y == 0.0) {
+      s.status = kBreakdown;
+      continue;
+    }
+    s.alpha = cdiv(s.rho, pq);
+    ++active;
+  }
+  *ctl.n_active = active;
+}
+
+template <int K>
+__device__ void fin_resid(const KrylovCtl& ctl, const double* tot) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+}
+
+template <int K>
+__device__ void fin_update(const KrylovCtl& ctl, const double* tot) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    if (s.status != kActive) continue;
+    const double2 rho_new = make_double2(tot[3 * k], tot[3 * k + 1]);
+    s.rnorm = sqrt(tot[3 * k + 2]);
+    s.iters += 1;
+    if (s.rnorm <= ctl.tol * s.bnorm) {
+      s.status = kConverged;
+    } else if (s.iters >= ctl.max_iter) {
+      s.status = kMaxIter;
+    } else if (rho_new.x == 0.0 && rho_new.y == 0.0) {
+      s.status = kBreakdown;
+    } else {
+      s.beta = cdiv(rho_new, s.rho);
+      s.rho = rho_new;
+      ++active;
+    }
+  }
+  *ctl.n_active = active;
+}
+
+template <int K>
+__device__ void fin_start(const KrylovCtl& ctl, const double* tot, unsigned mask, int fresh) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    if ((mask >> k) & 1u) {
+      if (fresh) {
+        s.bnorm = sqrt(tot[4 * k + 3]);
+        s.iters = 0;
+      }
+      s.rho = make_double2(tot[4 * k], tot[4 * k + 1]);
+      s.rnorm = sqrt(tot[4 * k + 2]);
+      if (fresh && s.bnorm == 0.0) {
+        s.status = kZeroRhs;
+      } else if (s.rnorm <= ctl.tol * s.bnorm) {
+        s.status = kConverged;
+      } else if (s.rho.x == 0.0 && s.rho.y == 0.0) {
+        s.status = kBreakdown;
+      } else {
+        s.status = kActive;
+      }
+    }
+    active += s.status == kActive;
+  }
+  *ctl.n_active = active;
+}
+
+enum Fin { kFinAlpha = 0, kFinUpdate = 1, kFinStart = 2, kFinResid = 3 };
+
+// Finalisation after a cross-part reduction of ctl.red (distributed solve).
+template <int K, int WHAT>
+__global__ void k_fin(KrylovCtl ctl, unsigned mask, int fresh) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  constexpr int NV = WHAT == kFinAlpha ? 2 * K : WHAT == kFinUpdate ? 3 * K
+                     : WHAT == kFinStart ? 4 * K : K;
+  if (WHAT != kFinStart && WHAT != kFinResid && *ctl.n_active == 0) return;
+  double tot[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) tot[j] = ctl.red[j];
+  if (WHAT == kFinAlpha) fin_alpha<K>(ctl, tot);
+  else if (WHAT == kFinUpdate) fin_update<K>(ctl, tot);
+  else if (WHAT == kFinStart) fin_start<K>(ctl, tot, mask, fresh);
+  else fin_resid<K>(ctl, tot);
+}
 
 // y = A x for K interleaved vectors with G lanes per row.
 //  kPlain: y = A x
@@ -223,24 +325,13 @@ k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
   if (threadIdx.x == 0) {
-    if (MODE == kCocg) {
-      int active = 0;
+    if (ctl.red) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        RhsState& s = ctl.st[k];
-        if (s.status != kActive) continue;
-        const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
-        if (pq.x == 0.0 && pq.y == 0.0) {
-          s.status = kBreakdown;
-          continue;
-        }
-        s.alpha = cdiv(s.rho, pq);
-        ++active;
-      }
-      *ctl.n_active = active;
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
     } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+      fin_resid<K>(ctl, tot);
     }
     *ctl.counter = 0u;
   }
@@ -267,7 +358,8 @@ struct NbView {
   const double* cpl;    // plane p of coupling q at cpl + 4 * (p * ncpl + q)
   int64_t ncpl;
   const int* cond_fwd;
-  int64_t n_nodes;
+  int64_t n_nodes;  // nodes whose rows this view computes (owned nodes)
+  int64_t na;       // V block offset in the x/y layout (3 n_nodes, or 3 (L + G) on a part)
 };
 
 // 256-bit streaming load (read-once matrix data: no L1 allocation)
@@ -338,7 +430,7 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   const int g = lane & (G - 1);
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t na = 3 * A.n_nodes;
+  const int64_t na = A.na;
   double part[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) part[j] = 0.0;
@@ -519,24 +611,13 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
   if (threadIdx.x == 0) {
-    if (MODE == kCocg) {
-      int active = 0;
+    if (ctl.red) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        RhsState& s = ctl.st[k];
-        if (s.status != kActive) continue;
-        const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
-        if (pq.x == 0.0 && pq.y == 0.0) {
-          s.status = kBreakdown;
-          continue;
-        }
-        s.alpha = cdiv(s.rho, pq);
-        ++active;
-      }
-      *ctl.n_active = active;
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
     } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+      fin_resid<K>(ctl, tot);
     }
     *ctl.counter = 0u;
   }
@@ -578,7 +659,7 @@ k_nbt_spmv(NbtView T, const double2* __restrict__ x, double2* __restrict__ y,
   const NbView& A = T.nb;
   const int lane = threadIdx.x & 31;
   const int g = lane & (G - 1);
-  const int64_t na = 3 * A.n_nodes;
+  const int64_t na = A.na;
   double part[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) part[j] = 0.0;
@@ -726,24 +807,13 @@ k_nbt_spmv(NbtView T, const double2* __restrict__ x, double2* __restrict__ y,
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
   if (threadIdx.x == 0) {
-    if (MODE == kCocg) {
-      int active = 0;
+    if (ctl.red) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        RhsState& s = ctl.st[k];
-        if (s.status != kActive) continue;
-        const double2 pq = make_double2(tot[2 * k], tot[2 * k + 1]);
-        if (pq.x == 0.0 && pq.y == 0.0) {
-          s.status = kBreakdown;
-          continue;
-        }
-        s.alpha = cdiv(s.rho, pq);
-        ++active;
-      }
-      *ctl.n_active = active;
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
     } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) ctl.st[k].rnorm = sqrt(tot[k]);
+      fin_resid<K>(ctl, tot);
     }
     *ctl.counter = 0u;
   }
@@ -943,8 +1013,10 @@ k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const doub
   double part[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) part[j] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
     const double2 d = dinv[i];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -970,27 +1042,12 @@ k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const doub
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
   if (threadIdx.x == 0) {
-    int active = 0;
+    if (ctl.red) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      RhsState& s = ctl.st[k];
-      if (s.status != kActive) continue;
-      const double2 rho_new = make_double2(tot[3 * k], tot[3 * k + 1]);
-      s.rnorm = sqrt(tot[3 * k + 2]);
-      s.iters += 1;
-      if (s.rnorm <= ctl.tol * s.bnorm) {
-        s.status = kConverged;
-      } else if (s.iters >= ctl.max_iter) {
-        s.status = kMaxIter;
-      } else if (rho_new.x == 0.0 && rho_new.y == 0.0) {
-        s.status = kBreakdown;
-      } else {
-        s.beta = cdiv(rho_new, s.rho);
-        s.rho = rho_new;
-        ++active;
-      }
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else {
+      fin_update<K>(ctl, tot);
     }
-    *ctl.n_active = active;
     *ctl.counter = 0u;
   }
 }
@@ -1008,8 +1065,10 @@ k_pupdate(int64_t n, const double2* __restrict__ r, double2* __restrict__ p,
     act[k] = ctl.st[k].status == kActive;
     beta[k] = ctl.st[k].beta;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
     const double2 d = dinv[i];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -1033,8 +1092,10 @@ k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, doubl
   double part[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) part[j] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
     const double2 d = dinv[i];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -1064,30 +1125,12 @@ k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, doubl
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
   if (threadIdx.x == 0) {
-    int active = 0;
+    if (ctl.red) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      RhsState& s = ctl.st[k];
-      if ((mask >> k) & 1u) {
-        if (fresh) {
-          s.bnorm = sqrt(tot[4 * k + 3]);
-          s.iters = 0;
-        }
-        s.rho = make_double2(tot[4 * k], tot[4 * k + 1]);
-        s.rnorm = sqrt(tot[4 * k + 2]);
-        if (fresh && s.bnorm == 0.0) {
-          s.status = kZeroRhs;
-        } else if (s.rnorm <= ctl.tol * s.bnorm) {
-          s.status = kConverged;
-        } else if (s.rho.x == 0.0 && s.rho.y == 0.0) {
-          s.status = kBreakdown;
-        } else {
-          s.status = kActive;
-        }
-      }
-      active += s.status == kActive;
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else {
+      fin_start<K>(ctl, tot, mask, fresh);
     }
-    *ctl.n_active = active;
     *ctl.counter = 0u;
   }
 }
@@ -1122,7 +1165,7 @@ NbView nb_view(const ect_matrix* a) {
   return NbView{a->nb_blk_ptr, a->nb_blk_col, reinterpret_cast<const double*>(a->nb_blk.p),
                 a->nb_blocks, a->nb_cpl_ptr.p, a->nb_cpl_idx.p,
                 reinterpret_cast<const double*>(a->nb_cpl.p), a->nb_ncpl, a->nb_cond_fwd,
-                a->n_nodes};
+                a->n_nodes, 3 * a->n_nodes};
 }
 
 constexpr int kNbG = 8;  // lanes per node in the NB SpMV
@@ -1474,7 +1517,8 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       CK(cudaMemcpy2DAsync(bb.p, kk * sizeof(double2), b, k * sizeof(double2),
                            k * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
     }
-    KrylovCtl ctl{st.p, n_active.p, counter.p, partial.p, opt.tol, opt.max_iter};
+    KrylovCtl ctl{st.p, n_active.p, counter.p, partial.p, opt.tol, opt.max_iter,
+                  nullptr, 0, n, n, n};
     const unsigned all = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
     DK::start(ctx, grid_v, n, bb.p, xx.p, r.p, p.p, a->dinv.p, all, 1, ctl);
     note_launch(ctx, 1);
@@ -1573,6 +1617,415 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
     }
     CK(cudaStreamSynchronize(s));
   });
+}
+
+
+// ============================================================================
+// Distributed (row-partitioned) solve — SURVEY §8(e), configs[4].
+// Each part owns a contiguous node range (dist_plan.cpp); per SpMV the ghost
+// x values are exchanged with the neighbour parts (NCCL send/recv, or device
+// copies when all parts run in this process on one GPU), and the per-iteration
+// dot products are summed across parts (ncclAllReduce of <= 4k doubles, or a
+// fixed-order device sum) before the scalar finalisation (k_fin). The
+// in-process mode runs exactly the same kernels and partition logic: it is how
+// the partitioned path is validated on a single GPU.
+namespace {
+
+__global__ void k_scatter_cols(const int* __restrict__ idx, int64_t n, const int* __restrict__ map,
+                               int* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = map[idx[i]];
+}
+
+template <int K>
+__global__ void k_pack(const double2* __restrict__ v, const int* __restrict__ nodes, int64_t ns,
+                       const int* __restrict__ cnodes, int64_t nsc,
+                       const int* __restrict__ cond_local, int64_t na_local, double2* out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ns * 3 * K; e += stride) {
+    const int64_t nd = e / (3 * K), c = e - nd * 3 * K;
+    out[e] = v[(int64_t)nodes[nd] * 3 * K + c];
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nsc * K; e += stride) {
+    const int64_t nd = e / K, k = e - nd * K;
+    out[ns * 3 * K + e] = v[(na_local + cond_local[cnodes[nd]]) * K + k];
+  }
+}
+
+// fixed-order sum of the parts' totals, broadcast back to every part
+__global__ void k_sum_parts(double* const* reds, int n_parts, int nv) {
+  for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n_parts; ++r) s += reds[r][j];
+    for (int r = 0; r < n_parts; ++r) reds[r][j] = s;
+  }
+}
+
+NbView part_view(const ect_part* P) {
+  return NbView{P->blk_ptr.p, P->blk_col.p, reinterpret_cast<const double*>(P->blk.p), P->nblk,
+                P->cpl_ptr.p, P->cpl_idx.p, reinterpret_cast<const double*>(P->cpl.p), P->ncpl,
+                P->cond_local.p, P->plan.L, P->plan.na_local()};
+}
+
+}  // namespace
+
+ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_parts, int part) {
+  ect_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  if (!a->has_nb) fail(ECT_ERR_SOLVER, "part: the global matrix must be assembled in NB format");
+  const int64_t nn = m->n_nodes;
+  // host copies of the neighbour structure, conductor map and NB coupling index
+  std::vector<int> nbr_off(nn + 1), cond(nn), cpl_ptr(nn + 1);
+  CK(cudaMemcpyAsync(nbr_off.data(), m->nbr_off.p, (nn + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(cond.data(), m->cond_fwd.p, nn * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(cpl_ptr.data(), a->nb_cpl_ptr.p, (nn + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<int> nbr(nbr_off[nn]);
+  CK(cudaMemcpy(nbr.data(), m->nbr.p, nbr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  auto P = std::make_unique<ect_part>();
+  P->ctx = ctx;
+  P->plan = build_halo_plan(nn, nbr_off.data(), nbr.data(), cond.data(), splits, n_parts, part);
+  const HaloPlan& H = P->plan;
+  P->n_nodes_global = nn;
+  P->na_global = 3 * nn;
+  P->n_global = 3 * nn + m->n_cond;
+  const int64_t L = H.L, G = H.G, NL = H.n_local();
+  // global node -> local node map (owned, ghosts; -1 elsewhere) on the device
+  std::vector<int> g2l(nn, -1);
+  for (int64_t i = 0; i < L; ++i) g2l[H.n0 + i] = (int)i;
+  for (int64_t q = 0; q < G; ++q) g2l[H.ghost_nodes[q]] = (int)(L + q);
+  DevBuf<int> d_g2l(nn);
+  CK(cudaMemcpy(d_g2l.p, g2l.data(), nn * sizeof(int), cudaMemcpyHostToDevice));
+  // blocks of the owned nodes: contiguous slice of the global NB arrays
+  const int64_t q0 = nbr_off[H.n0], q1 = nbr_off[H.n1];
+  P->nblk = q1 - q0;
+  P->blk_ptr.alloc(L + 1);
+  {
+    std::vector<int> bp(L + 1);
+    for (int64_t i = 0; i <= L; ++i) bp[i] = nbr_off[H.n0 + i] - (int)q0;
+    CK(cudaMemcpy(P->blk_ptr.p, bp.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  P->blk_col.alloc(std::max<int64_t>(1, P->nblk));
+  P->blk.alloc(6 * std::max<int64_t>(1, P->nblk));
+  if (P->nblk) {
+    k_scatter_cols<<<(int)std::min<int64_t>((P->nblk + 255) / 256, ctx->num_sms * 16), 256, 0, s>>>(
+        m->nbr.p + q0, P->nblk, d_g2l.p, P->blk_col.p);
+    CK_LAUNCH();
+    for (int pl = 0; pl < 3; ++pl)
+      CK(cudaMemcpyAsync(reinterpret_cast<double*>(P->blk.p) + 4 * pl * P->nblk,
+                         reinterpret_cast<const double*>(a->nb_blk.p) + 4 * (pl * a->nb_blocks + q0),
+                         4 * P->nblk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  // couplings of the owned nodes
+  const int64_t c0 = cpl_ptr[H.n0], c1 = cpl_ptr[H.n1];
+  P->ncpl = c1 - c0;
+  P->cpl_ptr.alloc(L + 1);
+  {
+    std::vector<int> cp(L + 1);
+    for (int64_t i = 0; i <= L; ++i) cp[i] = cpl_ptr[H.n0 + i] - (int)c0;
+    CK(cudaMemcpy(P->cpl_ptr.p, cp.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  P->cpl_idx.alloc(std::max<int64_t>(1, P->ncpl));
+  P->cpl.alloc(4 * std::max<int64_t>(1, P->ncpl));
+  if (P->ncpl) {
+    std::vector<int2> ci(P->ncpl);
+    CK(cudaMemcpy(ci.data(), a->nb_cpl_idx.p + c0, P->ncpl * sizeof(int2), cudaMemcpyDeviceToHost));
+    for (auto& e : ci) {
+      const int l = g2l[e.x];
+      e = make_int2(l, H.local_vdof[l]);
+    }
+    CK(cudaMemcpy(P->cpl_idx.p, ci.data(), P->ncpl * sizeof(int2), cudaMemcpyHostToDevice));
+    for (int pl = 0; pl < 2; ++pl)
+      CK(cudaMemcpyAsync(reinterpret_cast<double*>(P->cpl.p) + 4 * pl * P->ncpl,
+                         reinterpret_cast<const double*>(a->nb_cpl.p) + 4 * (pl * a->nb_ncpl + c0),
+                         4 * P->ncpl * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  P->cond_local.alloc(std::max<int64_t>(1, L + G));
+  CK(cudaMemcpy(P->cond_local.p, H.local_vdof.data(), (L + G) * sizeof(int), cudaMemcpyHostToDevice));
+  // Jacobi diagonal of the owned rows in the local layout (ghost rows unused)
+  P->dinv.alloc(NL);
+  CK(cudaMemsetAsync(P->dinv.p, 0, P->dinv.bytes(), s));
+  CK(cudaMemcpyAsync(P->dinv.p, a->dinv.p + 3 * H.n0, 3 * L * sizeof(double2),
+                     cudaMemcpyDeviceToDevice, s));
+  if (H.Vo)
+    CK(cudaMemcpyAsync(P->dinv.p + H.na_local(), a->dinv.p + 3 * nn + H.c0, H.Vo * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, s));
+  // send lists
+  for (const auto& peer : H.peers) {
+    ect_part::Peer d;
+    d.ns = (int64_t)peer.send_nodes.size();
+    d.nsc = (int64_t)peer.send_cond_nodes.size();
+    d.send_nodes.alloc(std::max<int64_t>(1, d.ns));
+    d.send_cond.alloc(std::max<int64_t>(1, d.nsc));
+    if (d.ns) CK(cudaMemcpy(d.send_nodes.p, peer.send_nodes.data(), d.ns * sizeof(int), cudaMemcpyHostToDevice));
+    if (d.nsc) CK(cudaMemcpy(d.send_cond.p, peer.send_cond_nodes.data(), d.nsc * sizeof(int), cudaMemcpyHostToDevice));
+    P->peers.push_back(std::move(d));
+  }
+  CK(cudaStreamSynchronize(s));
+  note_launch(ctx, 1);
+  return P.release();
+}
+
+namespace {
+
+template <int K>
+struct PartState {
+  DevBuf<double2> b, x, r, p, q;
+  DevBuf<RhsState> st;
+  DevBuf<int> n_active;
+  DevBuf<unsigned> counter;
+  DevBuf<double> partial, red;
+  KrylovCtl ctl{};
+};
+
+template <int K>
+void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_global,
+                  double2* x_global, int k, const ect_iter_options& opt, SolveOut* out) {
+  using DK = Dispatch<K>;
+  ect_ctx* ctx = parts[0]->ctx;
+  cudaStream_t s = ctx->stream;
+  for (int r = 0; r < R; ++r)
+    if (parts[r]->ctx != ctx) fail(ECT_ERR_SOLVER, "dist_solve: in-process parts must share a context");
+  if (comm && R != 1) fail(ECT_ERR_SOLVER, "dist_solve: with a communicator each process owns one part");
+  const int grid_s = grid_for(ctx, nb_fn<K>(ctx->nb_variant, kCocg), kBlock);
+  const int grid_v = DK::vec_grid(ctx);
+  const int grid_max = std::max(grid_s, grid_v);
+  const int64_t na_g = parts[0]->na_global;
+  std::vector<PartState<K>> S(R);
+  DevBuf<double*> reds(R);
+  std::vector<double*> h_reds(R);
+  for (int r = 0; r < R; ++r) {
+    const HaloPlan& H = parts[r]->plan;
+    const int64_t NL = H.n_local();
+    PartState<K>& P = S[r];
+    P.b.alloc(NL * K); P.x.alloc(NL * K); P.r.alloc(NL * K); P.p.alloc(NL * K); P.q.alloc(NL * K);
+    for (auto* v : {&P.b, &P.x, &P.r, &P.p, &P.q}) CK(cudaMemsetAsync(v->p, 0, v->bytes(), s));
+    P.st.alloc(K); P.n_active.alloc(1); P.counter.alloc(1);
+    P.partial.alloc((size_t)grid_max * 4 * K); P.red.alloc(4 * K);
+    CK(cudaMemsetAsync(P.st.p, 0, P.st.bytes(), s));
+    CK(cudaMemsetAsync(P.counter.p, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(P.n_active.p, 0, sizeof(int), s));
+    P.ctl = KrylovCtl{P.st.p, P.n_active.p, P.counter.p, P.partial.p, opt.tol, opt.max_iter,
+                      P.red.p, 0, 3 * H.L, H.na_local(), H.na_local() + H.Vo};
+    // owned rows of b: A rows [3 n0, 3 n1), V rows [na + c0, na + c0 + Vo)
+    CK(cudaMemcpyAsync(P.b.p, b_global + 3 * H.n0 * K, 3 * H.L * K * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, s));
+    if (H.Vo)
+      CK(cudaMemcpyAsync(P.b.p + H.na_local() * K, b_global + (na_g + H.c0) * K,
+                         H.Vo * K * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    h_reds[r] = P.red.p;
+  }
+  CK(cudaMemcpyAsync(reds.p, h_reds.data(), R * sizeof(double*), cudaMemcpyHostToDevice, s));
+
+  auto allreduce = [&](int nv) {
+    if (comm) nccl_allreduce_sum(comm, S[0].red.p, nv, s);
+    else if (R > 1) { k_sum_parts<<<1, 64, 0, s>>>(reds.p, R, nv); CK_LAUNCH(); }
+  };
+  // ghost exchange of vector v (member pointer of PartState)
+  auto halo = [&](DevBuf<double2> PartState<K>::*v) {
+    for (int r = 0; r < R; ++r) {
+      ect_part* P = parts[r];
+      for (size_t i = 0; i < P->peers.size(); ++i) {
+        auto& d = P->peers[i];
+        const int64_t cnt = d.ns * 3 * K + d.nsc * K;
+        d.sendbuf.ensure(std::max<int64_t>(1, cnt));
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((cnt + 255) / 256, ctx->num_sms * 8));
+        k_pack<K><<<g, 256, 0, s>>>((S[r].*v).p, d.send_nodes.p, d.ns, d.send_cond.p, d.nsc,
+                                    P->cond_local.p, P->plan.na_local(), d.sendbuf.p);
+        CK_LAUNCH();
+      }
+    }
+    if (comm) nccl_group_start();
+    for (int r = 0; r < R; ++r) {
+      ect_part* P = parts[r];
+      const HaloPlan& H = P->plan;
+      double2* base = (S[r].*v).p;
+      for (size_t i = 0; i < H.peers.size(); ++i) {
+        const HaloPeer& hp = H.peers[i];
+        double2* dstA = base + 3 * (H.L + hp.recv_node_begin) * K;
+        double2* dstV = base + (H.na_local() + H.Vo + hp.recv_v_begin) * K;
+        if (comm) {
+          const auto& d = P->peers[i];
+          nccl_send(comm, d.sendbuf.p, 2 * d.ns * 3 * K, hp.part, s);
+          if (d.nsc) nccl_send(comm, d.sendbuf.p + d.ns * 3 * K, 2 * d.nsc * K, hp.part, s);
+          nccl_recv(comm, dstA, 2 * hp.recv_node_count * 3 * K, hp.part, s);
+          if (hp.recv_v_count) nccl_recv(comm, dstV, 2 * hp.recv_v_count * K, hp.part, s);
+        } else {
+          // the owner's send buffer for this part
+          ect_part* Q = parts[hp.part];
+          size_t qi = 0;
+          while (qi < Q->plan.peers.size() && Q->plan.peers[qi].part != r) ++qi;
+          if (qi == Q->plan.peers.size()) fail(ECT_ERR_SOLVER, "halo plan: asymmetric peers");
+          const auto& d = Q->peers[qi];
+          if (d.ns != hp.recv_node_count || d.nsc != hp.recv_v_count)
+            fail(ECT_ERR_SOLVER, "halo plan: send/receive sizes differ");
+          CK(cudaMemcpyAsync(dstA, d.sendbuf.p, d.ns * 3 * K * sizeof(double2),
+                             cudaMemcpyDeviceToDevice, s));
+          if (d.nsc)
+            CK(cudaMemcpyAsync(dstV, d.sendbuf.p + d.ns * 3 * K, d.nsc * K * sizeof(double2),
+                               cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    }
+    if (comm) nccl_group_end();
+  };
+  auto spmv = [&](int mode, DevBuf<double2> PartState<K>::*xin, DevBuf<double2> PartState<K>::*yout,
+                  bool with_b) {
+    for (int r = 0; r < R; ++r) {
+      NbView v = part_view(parts[r]);
+      const double2* xp = (S[r].*xin).p;
+      double2* yp = (S[r].*yout).p;
+      const double2* bp = with_b ? S[r].b.p : nullptr;
+      KrylovCtl c = S[r].ctl;
+      void* args[] = {&v, &xp, &yp, &bp, &c};
+      CK(cudaLaunchKernel(nb_fn<K>(ctx->nb_variant, mode), dim3(grid_s), dim3(kBlock), args, 0, s));
+    }
+  };
+  auto fin = [&](int what, unsigned mask, int fresh) {
+    for (int r = 0; r < R; ++r) {
+      KrylovCtl c = S[r].ctl;
+      if (what == kFinAlpha) k_fin<K, kFinAlpha><<<1, 32, 0, s>>>(c, mask, fresh);
+      else if (what == kFinUpdate) k_fin<K, kFinUpdate><<<1, 32, 0, s>>>(c, mask, fresh);
+      else if (what == kFinStart) k_fin<K, kFinStart><<<1, 32, 0, s>>>(c, mask, fresh);
+      else k_fin<K, kFinResid><<<1, 32, 0, s>>>(c, mask, fresh);
+      CK_LAUNCH();
+    }
+  };
+  auto start = [&](unsigned mask, int fresh) {
+    for (int r = 0; r < R; ++r) {
+      const HaloPlan& H = parts[r]->plan;
+      DK::start(ctx, grid_v, H.n_local(), S[r].b.p, S[r].x.p, S[r].r.p, S[r].p.p, parts[r]->dinv.p,
+                mask, fresh, S[r].ctl);
+    }
+    allreduce(4 * K);
+    fin(kFinStart, mask, fresh);
+  };
+
+  const unsigned all = (K == 32) ? 0xffffffffu : ((1u << K) - 1u);
+  start(all, 1);
+  out->iters.assign(k, 0);
+  out->residual.assign(k, 0.0);
+  out->converged.assign(k, 0);
+  std::vector<RhsState> hs(K);
+  int* flag = ctx->pinned_flag;
+  const int chunk = 16;
+  for (int round = 0;; ++round) {
+    for (int launched = 0; opt.max_iter > 0 && launched <= opt.max_iter + chunk;) {
+      for (int it = 0; it < chunk; ++it) {
+        halo(&PartState<K>::p);
+        spmv(kCocg, &PartState<K>::p, &PartState<K>::q, false);
+        allreduce(2 * K);
+        fin(kFinAlpha, 0, 0);
+        for (int r = 0; r < R; ++r)
+          DK::update(ctx, grid_v, parts[r]->plan.n_local(), S[r].x.p, S[r].r.p, S[r].p.p,
+                     S[r].q.p, parts[r]->dinv.p, S[r].ctl);
+        allreduce(3 * K);
+        fin(kFinUpdate, 0, 0);
+        for (int r = 0; r < R; ++r)
+          DK::pupdate(ctx, grid_v, parts[r]->plan.n_local(), S[r].r.p, S[r].p.p, parts[r]->dinv.p,
+                      S[r].ctl);
+      }
+      launched += chunk;
+      CK(cudaMemcpyAsync(flag, S[0].n_active.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (*flag == 0) break;
+    }
+    // true residual (iterative.cpp:208-216): q <- b - A x, norms across parts
+    CK(cudaMemcpyAsync(hs.data(), S[0].st.p, K * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));  // statuses are identical on every part
+    {
+      std::vector<RhsState> tmp = hs;
+      for (auto& t : tmp) t.status = kActive;
+      for (int r = 0; r < R; ++r) {
+        CK(cudaMemcpyAsync(S[r].st.p, tmp.data(), K * sizeof(RhsState), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(S[r].n_active.p, 0xff, sizeof(int), s));
+      }
+      CK(cudaStreamSynchronize(s));
+    }
+    halo(&PartState<K>::x);
+    spmv(kResid, &PartState<K>::x, &PartState<K>::q, true);
+    allreduce(K);
+    fin(kFinResid, 0, 0);
+    std::vector<RhsState> res(K);
+    CK(cudaMemcpyAsync(res.data(), S[0].st.p, K * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < K; ++c) hs[c].rnorm = res[c].rnorm;  // keep statuses, true norm
+    for (int r = 0; r < R; ++r)
+      CK(cudaMemcpyAsync(S[r].st.p, hs.data(), K * sizeof(RhsState), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    unsigned restart_mask = 0;
+    for (int c = 0; c < k; ++c) {
+      const RhsState& t = hs[c];
+      if (t.status == kBreakdown) fail(ECT_ERR_SOLVER, "COCG breakdown on right-hand side " + std::to_string(c));
+      const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
+      if (t.status == kConverged && rel > opt.tol && t.iters < opt.max_iter && round < 8)
+        restart_mask |= 1u << c;
+    }
+    if (!restart_mask) break;
+    for (int r = 0; r < R; ++r)
+      for (int c = 0; c < K; ++c)
+        if ((restart_mask >> c) & 1u)
+          CK(cudaMemcpy2DAsync(S[r].r.p + c, K * sizeof(double2), S[r].q.p + c, K * sizeof(double2),
+                               sizeof(double2), parts[r]->plan.n_local(), cudaMemcpyDeviceToDevice, s));
+    start(restart_mask, 0);
+  }
+  for (int c = 0; c < k; ++c) {
+    const RhsState& t = hs[c];
+    out->iters[c] = t.iters;
+    const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
+    out->residual[c] = rel;
+    out->converged[c] = (t.status == kZeroRhs) || (t.status == kConverged && rel <= opt.tol);
+  }
+  // owned rows of x back to the global vector
+  for (int r = 0; r < R; ++r) {
+    const HaloPlan& H = parts[r]->plan;
+    CK(cudaMemcpyAsync(x_global + 3 * H.n0 * K, S[r].x.p, 3 * H.L * K * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, s));
+    if (H.Vo)
+      CK(cudaMemcpyAsync(x_global + (na_g + H.c0) * K, S[r].x.p + H.na_local() * K,
+                         H.Vo * K * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+void dist_solve(ect_part** parts, int n_parts, ect_comm* comm, const double2* b_global,
+                double2* x_global, int k, const ect_iter_options& opt, SolveOut* out) {
+  if (!(opt.tol > 0.0)) fail(ECT_ERR_SOLVER, "solve_iterative: tolerance must be positive");
+  if (n_parts < 1) fail(ECT_ERR_SOLVER, "dist_solve: no parts");
+  int kk = 1;
+  while (kk < k) kk <<= 1;
+  if (kk > 8) fail(ECT_ERR_SOLVER, "dist_solve: n_rhs must be in 1..8");
+  const int64_t n = parts[0]->n_global;
+  ect_ctx* ctx = parts[0]->ctx;
+  cudaStream_t s = ctx->stream;
+  // internal (power-of-two) batch width
+  DevBuf<double2> bpad, xpad;
+  const double2* bg = b_global;
+  double2* xg = x_global;
+  if (kk != k) {
+    bpad.alloc((size_t)n * kk);
+    xpad.alloc((size_t)n * kk);
+    CK(cudaMemsetAsync(bpad.p, 0, bpad.bytes(), s));
+    CK(cudaMemsetAsync(xpad.p, 0, xpad.bytes(), s));
+    CK(cudaMemcpy2DAsync(bpad.p, kk * sizeof(double2), b_global, k * sizeof(double2),
+                         k * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+    bg = bpad.p;
+    xg = xpad.p;
+  }
+  switch (kk) {
+    case 1: dist_solve_k<1>(parts, n_parts, comm, bg, xg, k, opt, out); break;
+    case 2: dist_solve_k<2>(parts, n_parts, comm, bg, xg, k, opt, out); break;
+    case 4: dist_solve_k<4>(parts, n_parts, comm, bg, xg, k, opt, out); break;
+    default: dist_solve_k<8>(parts, n_parts, comm, bg, xg, k, opt, out); break;
+  }
+  if (kk != k) {
+    CK(cudaMemcpy2DAsync(x_global, k * sizeof(double2), xpad.p, kk * sizeof(double2),
+                         k * sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
 }
 
 }  // namespace ect

@@ -338,3 +338,96 @@ class Session:
                         "z_f3": complex(p.z_f3[0], p.z_f3[1]), "failed": bool(p.failed),
                         "iterations": list(p.iterations)})
         return out
+
+
+# ---- distributed solve (row partition over GPUs) -------------------
+class HaloPlan:
+    """Host-only halo plan of one part (ect_halo_plan_*; no GPU needed)."""
+
+    def __init__(self, n_nodes, nbr_off, nbr, cond_fwd, splits, part):
+        nbr_off = np.ascontiguousarray(nbr_off, np.int32)
+        nbr = np.ascontiguousarray(nbr, np.int32)
+        cond_fwd = np.ascontiguousarray(cond_fwd, np.int32)
+        splits = np.ascontiguousarray(splits, np.int64)
+        h = VP()
+        _check(lib().ect_halo_plan_create(I64(n_nodes), _ptr(nbr_off), _ptr(nbr), _ptr(cond_fwd),
+                                          _ptr(splits), I32(len(splits) - 1), I32(part),
+                                          C.byref(h)))
+        self.h = h
+        info = (I64 * 8)()
+        _check(lib().ect_halo_plan_info(h, info))
+        (self.n0, self.n1, self.L, self.G, self.c0, self.Vo, self.Vg, n_peers) = list(info)
+        self.ghost_nodes = np.empty(self.G, np.int32)
+        self.local_vdof = np.empty(self.L + self.G, np.int32)
+        _check(lib().ect_halo_plan_arrays(h, _ptr(self.ghost_nodes), _ptr(self.local_vdof)))
+        self.peers = []
+        for i in range(n_peers):
+            pi = (I64 * 7)()
+            _check(lib().ect_halo_plan_peer(h, I32(i), pi, None, None))
+            sn = np.empty(pi[5], np.int32)
+            sc = np.empty(pi[6], np.int32)
+            _check(lib().ect_halo_plan_peer(h, I32(i), pi, _ptr(sn), _ptr(sc)))
+            self.peers.append({"part": pi[0], "recv_node_begin": pi[1], "recv_node_count": pi[2],
+                               "recv_v_begin": pi[3], "recv_v_count": pi[4],
+                               "send_nodes": sn, "send_cond_nodes": sc})
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ect_halo_plan_destroy(self.h)
+            self.h = None
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().ect_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """NCCL communicator for one rank of the distributed solve."""
+
+    def __init__(self, ctx: Context, rank: int, world: int, unique_id: bytes):
+        h = VP()
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        _check(lib().ect_comm_create(ctx.h, I32(rank), I32(world), buf, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ect_comm_destroy(self.h)
+            self.h = None
+
+
+class Part:
+    """Rows of nodes [splits[part], splits[part+1]) of an assembled matrix."""
+
+    def __init__(self, ctx: Context, mesh: Mesh, matrix: Matrix, splits, part: int):
+        splits = np.ascontiguousarray(splits, np.int64)
+        h = VP()
+        _check(lib().ect_part_create(ctx.h, mesh.h, matrix.h, _ptr(splits), I32(len(splits) - 1),
+                                     I32(part), C.byref(h)))
+        self.h, self.ctx = h, ctx
+        info = (I64 * 8)()
+        _check(lib().ect_part_info(h, info))
+        self.info = dict(zip(["n0", "n1", "L", "G", "Vo", "Vg", "n_peers", "n_blocks"], list(info)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ect_part_destroy(self.h)
+            self.h = None
+
+
+def dist_solve(parts, b, comm=None, tol=1e-8, max_iter=500, restart=80, out=None):
+    """Partitioned Jacobi-COCG on global b ([n] or [n, k]); returns (x, results).
+    comm=None runs every part in this process (one GPU); else one part/rank."""
+    k = 1 if b.ndim == 1 else b.shape[1]
+    bs = b if hasattr(b, "data_ptr") else np.ascontiguousarray(b, np.complex128)
+    if out is None:
+        out = np.zeros_like(bs) if not hasattr(b, "data_ptr") else b.new_zeros(b.shape)
+    arr = (VP * len(parts))(*[p.h for p in parts])
+    opts = IterOptions(tol, max_iter, restart)
+    res = (IterResult * k)()
+    _check(lib().ect_dist_solve(arr, I32(len(parts)), comm.h if comm else None, _ptr(bs), _ptr(out),
+                                I32(k), C.byref(opts), res))
+    return out, [{"iterations": r.iterations, "residual": r.residual,
+                  "converged": bool(r.converged)} for r in res]
