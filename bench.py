@@ -242,7 +242,9 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"k_nb_spmv (node-block, k={k} interleaved RHS, fused p^T q)"
                                    if nb["format"] != "csr" else f"k_spmv (CSR, k={k})",
-                         "mean_launch_ms": spmv_ms, "launches": int(tm["spmv_launches"]),
+                         "mean_launch_ms": spmv_ms,
+                         "launches_timed": int(tm["spmv_launches"]),
+                         "launch_sampling": "CUDA events on every 8th solver iteration",
                          "algorithmic_bytes": b_spmv,
                          "algorithmic_bytes_note": "SURVEY 8(d) CSR formula 20*nnz+4*(N+1)+32*k*N; "
                                                    "NB stores the same matrix in fewer bytes",

@@ -101,6 +101,13 @@ struct ect_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
   bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
+  struct SolverWorkspace {                      // cocg_solve buffers, reused across solves
+    ect::DevBuf<double2> bb, xx, r, p, q;
+    ect::DevBuf<ect::RhsState> st;
+    ect::DevBuf<int> n_active;
+    ect::DevBuf<unsigned> counter;
+    ect::DevBuf<double> partial;
+  } ws;
   bool no_tiles = true;                         // NB-T only with ect_ctx_set_format(ECT_FORMAT_NB_TILED)
   int nb_variant = 0;                           // NB SpMV kernel variant (ECT_NB_VARIANT)
 };

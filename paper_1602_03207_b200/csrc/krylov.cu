@@ -1201,6 +1201,8 @@ const void* nb_fn(int variant, int mode) {
       case 3: return ECT_NBF(4, 3);
       case 4: return ECT_NBF(8, 2);
       case 6: return ECT_NBF(8, 1);
+      case 7: return ECT_NBF(2, 2);
+      case 8: return ECT_NBF(2, 1);
       default: return ECT_NBF(4, 2);  // measured best on B200 (configs[1], k = 1, 2)
     }
   }
@@ -1301,9 +1303,14 @@ void with_k(int k, F&& fn) {
 }
 
 // kind 0: SpMV launches, kind 1: the fused vector-update launches.
-void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0) {
+// sampled = true (solver loop): time one launch in kProfStride, so the event
+// records do not perturb the timed region; the mean is over the sampled ones.
+constexpr int kProfStride = 8;
+void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0, bool sampled = false) {
+  ev[0] = ev[1] = nullptr;
   if (!ctx->prof.enabled) return;
   auto& P = ctx->prof;
+  if (sampled && (P.launches++ % kProfStride) != 0) return;
   if (P.used + 2 > P.pool.size()) {
     for (int i = 0; i < 512; ++i) {
       cudaEvent_t e;
@@ -1318,7 +1325,7 @@ void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0) {
   CK(cudaEventRecord(ev[0], ctx->stream));
 }
 void prof_end(ect_ctx* ctx, cudaEvent_t* ev) {
-  if (!ctx->prof.enabled) return;
+  if (!ctx->prof.enabled || ev[0] == nullptr) return;
   CK(cudaEventRecord(ev[1], ctx->stream));
 }
 void prof_collect(ect_ctx* ctx) {
@@ -1501,11 +1508,18 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
     const int grid_v = DK::vec_grid(ctx);
     const int grid_max = std::max(std::max(grid_s, grid_r), grid_v);
     const size_t vec = (size_t)n * kk;
-    DevBuf<double2> bb(vec), xx(vec), r(vec), p(vec), q(vec);
-    DevBuf<RhsState> st(kk);
-    DevBuf<int> n_active(1);
-    DevBuf<unsigned> counter(1);
-    DevBuf<double> partial((size_t)grid_max * 4 * kk);
+    // workspace cached on the context (a sweep solves thousands of times)
+    auto& W = ctx->ws;
+    for (auto* v : {&W.bb, &W.xx, &W.r, &W.p, &W.q}) v->ensure(vec);
+    W.st.ensure(kk);
+    W.n_active.ensure(1);
+    W.counter.ensure(1);
+    W.partial.ensure((size_t)grid_max * 4 * kk);
+    auto &bb = W.bb, &xx = W.xx, &r = W.r, &p = W.p, &q = W.q;
+    auto& st = W.st;
+    auto& n_active = W.n_active;
+    auto& counter = W.counter;
+    auto& partial = W.partial;
     CK(cudaMemsetAsync(st.p, 0, st.bytes(), s));
     CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), s));
     CK(cudaMemsetAsync(n_active.p, 0, sizeof(int), s));
@@ -1535,11 +1549,12 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       for (; opt.max_iter > 0;) {
         for (int it = 0; it < chunk; ++it) {
           cudaEvent_t ev[2];
-          prof_begin(ctx, ev);
+          prof_begin(ctx, ev, 0, true);
           DK::spmv(ctx, kCocg, grid_s, n, a, p.p, q.p, nullptr, ctl);
           prof_end(ctx, ev);
           cudaEvent_t ev2[2];
-          prof_begin(ctx, ev2, 1);
+          ev2[0] = ev2[1] = nullptr;
+          if (ev[0]) prof_begin(ctx, ev2, 1);  // same sampled iterations as the SpMV
           DK::update(ctx, grid_v, n, xx.p, r.p, p.p, q.p, a->dinv.p, ctl);
           DK::pupdate(ctx, grid_v, n, r.p, p.p, a->dinv.p, ctl);
           prof_end(ctx, ev2);
