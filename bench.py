@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "large"],
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "large", "micro"],
                     help="sweep: configs[1] mesh, configs[3] positions sharded over GPUs (weak); "
                          "large: configs[4] one system row-partitioned over GPUs (strong)")
     return ap.parse_args()
@@ -365,6 +365,50 @@ def run_reference(args):
     }), flush=True)
 
 
+def run_micro(args):
+    """configs[2]: 200 fixed Krylov iterations on the assembled configs[1]
+    matrix, right-hand side re/im uniform [-1, 1] from seed 2, CSR vs NB."""
+    import torch
+    from paper_1602_03207_b200 import ect, workloads
+    w = workloads.config1()
+    m = w.mesh()
+    ctx = ect.Context(0)
+    mesh = ect.Mesh(ctx, m.xyz, m.tets, m.region)
+    p, _, _ = mesh.materials(w.physics)
+    rng = np.random.default_rng(2)
+    out = {}
+    for fmt in ("nb", "csr"):
+        ctx.set_format(fmt)
+        a = ect.Matrix(ctx, mesh).assemble(p)
+        n = a.n
+        b = torch.from_numpy(rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)).cuda()
+        x = torch.empty_like(b)
+        a.solve(b, tol=1e-30, max_iter=20, out=x)  # warm
+        ctx.timings(reset=True)
+        ctx.set_profiling(True)
+        ctx.mark(0)
+        _, res = a.solve(b, tol=1e-30, max_iter=200, out=x)
+        ctx.mark(1)
+        ms = ctx.elapsed_ms(0, 1)
+        ctx.set_profiling(False)
+        tm = ctx.timings(reset=True)
+        spmv = tm["spmv_ms_total"] / max(1, tm["spmv_launches"])
+        B = 20 * a.nnz + 4 * (n + 1) + 32 * n
+        out[fmt] = {"iterations": res[0]["iterations"], "ms_per_iteration": ms / res[0]["iterations"],
+                    "spmv_ms": spmv, "spmv_algorithmic_GBps": B / spmv / 1e6,
+                    "dof_iter_per_s": n * res[0]["iterations"] / (ms / 1e3)}
+        del a
+    peak, src = measured_peak()
+    nbv = out["nb"]
+    print(json.dumps({"metric": METRIC, "value": nbv["dof_iter_per_s"], "unit": UNIT, "n_gpus": 1,
+                      "steps": 1, "warmup": 1, "ms_per_step": nbv["ms_per_iteration"] * 200,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                      "dtype": "f64", "data": "synthetic (configs[2]: x re/im U[-1,1], seed 2)",
+                      "config": {"workload": "configs[2] 200 fixed Jacobi-COCG iterations on the "
+                                             "configs[1] matrix", "formats": out,
+                                 "peak_GBps": peak, "peak_source": src}}), flush=True)
+
+
 def run_large(args):
     """configs[4]: one 27.4M-DOF system, rows partitioned by slabs of i-planes
     over the GPUs (NCCL halo per SpMV + allreduce per dot), strong scaling."""
@@ -434,5 +478,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.workload == "large":
         run_large(a)
+    elif a.workload == "micro":
+        run_micro(a)
     else:
         run_ours(a)

@@ -456,7 +456,7 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
         load_block(A, q, B_nx, Im_nx);
       }
       // (wide batches keep the accumulators for K right-hand sides instead)
-      constexpr bool kPipe = K <= 2;
+      constexpr bool kPipe = K <= 2 && MINB <= 2;
       for (; q < be; q += G) {
         int m = m_nx;
         double B[3][3], Im[3];
@@ -1197,13 +1197,16 @@ const void* nb_fn(int variant, int mode) {
   if constexpr (K <= 4) {
     switch (variant) {
       case 1: return ECT_NBF(4, 1);
-      case 2: return ECT_NBF(8, 3);
-      case 3: return ECT_NBF(4, 3);
       case 4: return ECT_NBF(8, 2);
       case 6: return ECT_NBF(8, 1);
       case 7: return ECT_NBF(2, 2);
+      case 9: return ECT_NBF(1, 2);
       case 8: return ECT_NBF(2, 1);
-      default: return ECT_NBF(4, 2);  // measured best on B200 (configs[1], k = 1, 2)
+      case 10: return ECT_NBF(4, 2);
+      case 11: return ECT_NBF(2, 3);
+      case 12: return ECT_NBF(4, 3);
+      case 13: return ECT_NBF(2, 4);
+      default: return ECT_NBF(2, 2);  // measured best on B200 (configs[1], k = 1, 2, 4)
     }
   }
   return ECT_NBF(8, 1);
