@@ -88,6 +88,31 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
   __syncthreads();
 }
 
+// Block-wide sum when lane l holds NVL values of slot (l % CL): the result in
+// thread 0's out[NVL * CL] is ordered slot-major (fixed order, deterministic).
+template <int NVL, int CL>
+__device__ __forceinline__ void block_sum_slots(double (&v)[NVL], double* smem,
+                                                double (&out)[NVL * CL]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NVL; ++j)
+#pragma unroll
+    for (int o = 16; o >= CL; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+  if (lane < CL)
+#pragma unroll
+    for (int j = 0; j < NVL; ++j) smem[(wid * CL + lane) * NVL + j] = v[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NVL * CL; ++j) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += smem[w * NVL * CL + j];
+      out[j] = t;
+    }
+  }
+  __syncthreads();
+}
+
 // Last-block-done: returns true in the block that finished last (all of
 // whose threads then see every other block's partials).
 __device__ __forceinline__ bool last_block(unsigned* counter) {
@@ -415,32 +440,44 @@ __device__ __forceinline__ int2 ldg_i2(const int2* p) {
   return v;
 }
 
-template <int G, int K, int MODE, int MINB = 1>
+// G lanes per node = GB block lanes x CL column lanes. Block lane bl streams
+// the node's blocks bl, bl + GB, ...; column lane cl computes the KL = K / CL
+// right-hand sides [cl KL, (cl + 1) KL). CL > 1 keeps the per-lane state of a
+// narrow batch for a wide one (the CL lanes of one block load the same
+// addresses in the same instruction: one request), so wide batches keep the
+// software pipeline and 128-register occupancy instead of spilling.
+template <int G, int K, int MODE, int MINB = 1, int CL = 1>
 __global__ void __launch_bounds__(kBlock, MINB)
 k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           const double2* __restrict__ b, KrylovCtl ctl) {
-  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
+  static_assert(G % CL == 0 && K % CL == 0, "lane split");
+  constexpr int GB = G / CL;   // block lanes per node
+  constexpr int KL = K / CL;   // right-hand sides per lane
+  constexpr int NVL = (MODE == kCocg) ? 2 * KL : (MODE == kResid ? KL : 1);  // per lane
+  constexpr int NV = NVL * CL;
   __shared__ double smem[32 * (NV > 0 ? NV : 1)];
   if (MODE != kPlain && *ctl.n_active == 0) return;
-  bool act[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) act[k] = (MODE == kPlain) || ctl.st[k].status == kActive;
   constexpr int NPW = 32 / G;  // nodes per warp and pass
   const int lane = threadIdx.x & 31;
   const int g = lane & (G - 1);
+  const int bl = g / CL, cl = g % CL;
+  const int kc = cl * KL;      // first column of this lane
+  bool act[KL];
+#pragma unroll
+  for (int k = 0; k < KL; ++k) act[k] = (MODE == kPlain) || ctl.st[kc + k].status == kActive;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t na = A.na;
-  double part[NV];
+  double part[NVL];  // this lane's columns [kc, kc + KL)
 #pragma unroll
-  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
 
   for (int64_t wn = warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
     const int64_t i = wn + lane / G;
     const bool valid = i < A.n_nodes;
-    double2 acc[3][K], accv[K];
+    double2 acc[3][KL], accv[KL];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < KL; ++k) {
       acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
     }
     int cf_i = -1;
@@ -448,16 +485,16 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       const int be = A.blk_ptr[i + 1];
       // software pipeline: the next block's column and planes are in flight
       // while this block's x gathers and FMAs run (latency-bound otherwise)
-      int q = A.blk_ptr[i] + g;
+      int q = A.blk_ptr[i] + bl;
       int m_nx = 0;
       double B_nx[3][3], Im_nx[3];
       if (q < be) {
         m_nx = ldg_i(A.blk_col + q);
         load_block(A, q, B_nx, Im_nx);
       }
-      // (wide batches keep the accumulators for K right-hand sides instead)
-      constexpr bool kPipe = K <= 2 && MINB <= 2;
-      for (; q < be; q += G) {
+      // (wide per-lane batches keep the accumulators instead)
+      constexpr bool kPipe = KL <= 2 && MINB <= 2;
+      for (; q < be; q += GB) {
         int m = m_nx;
         double B[3][3], Im[3];
         if constexpr (kPipe) {
@@ -467,12 +504,12 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
 #pragma unroll
             for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
           }
-          if (q + G < be) {
-            m_nx = ldg_i(A.blk_col + q + G);
-            load_block(A, q + G, B_nx, Im_nx);
+          if (q + GB < be) {
+            m_nx = ldg_i(A.blk_col + q + GB);
+            load_block(A, q + GB, B_nx, Im_nx);
           }
         } else {
-          if (q != A.blk_ptr[i] + g) {
+          if (q != A.blk_ptr[i] + bl) {
             m = ldg_i(A.blk_col + q);
             load_block(A, q, B, Im);
           } else {
@@ -484,11 +521,11 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
             }
           }
         }
-        const double2* xm = x + (int64_t)3 * m * K;
+        const double2* xm = x + (int64_t)3 * m * K + kc;
         // right-hand sides in pairs: one 256-bit gather per (component, pair)
-        constexpr int KP = (K % 2 == 0) ? 2 : 1;
+        constexpr int KP = (KL % 2 == 0) ? 2 : 1;
 #pragma unroll
-        for (int k0 = 0; k0 < K; k0 += KP) {
+        for (int k0 = 0; k0 < KL; k0 += KP) {
           if (!act[k0] && !act[k0 + KP - 1]) continue;
           double2 xp[3][KP];
 #pragma unroll
@@ -517,16 +554,16 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       cf_i = A.cond_fwd[i];
       if (cf_i >= 0) {
         const int ce = A.cpl_ptr[i + 1];
-        for (int q = A.cpl_ptr[i] + g; q < ce; q += G) {
+        for (int q = A.cpl_ptr[i] + bl; q < ce; q += GB) {
           const int2 mi = ldg_i2(A.cpl_idx + q);
           double av[3], va[3];
           double2 Q3;
           load_cpl(A, q, av, va, Q3);
-          const double2* xm = x + (int64_t)3 * mi.x * K;
-          const double2* xvp = x + (na + mi.y) * K;
-          constexpr int KP = (K % 2 == 0) ? 2 : 1;
+          const double2* xm = x + (int64_t)3 * mi.x * K + kc;
+          const double2* xvp = x + (na + mi.y) * K + kc;
+          constexpr int KP = (KL % 2 == 0) ? 2 : 1;
 #pragma unroll
-          for (int k0 = 0; k0 < K; k0 += KP) {
+          for (int k0 = 0; k0 < KL; k0 += KP) {
             if (!act[k0] && !act[k0 + KP - 1]) continue;
             double2 xa[3][KP], xv[KP];
             if constexpr (KP == 2) {
@@ -561,11 +598,11 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
         }
       }
     }
-    // segment reduction over the G lanes of a node
+    // segment reduction over the GB block lanes of a node (same column lane)
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < KL; ++k) {
 #pragma unroll
-      for (int o = G / 2; o; o >>= 1) {
+      for (int o = (GB / 2) * CL; o >= CL; o >>= 1) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
@@ -575,16 +612,16 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
         accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
       }
     }
-    if (g == 0 && valid) {
+    if (bl == 0 && valid) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
+      for (int k = 0; k < KL; ++k) {
         if (!act[k]) continue;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (c == 3 && cf_i < 0) break;
           const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
           const double2 v = c < 3 ? acc[c][k] : accv[k];
-          const int64_t idx = row * K + k;
+          const int64_t idx = row * K + kc + k;
           if (MODE == kPlain) {
             y[idx] = v;
           } else if (MODE == kCocg) {
@@ -603,10 +640,12 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   }
   if (MODE == kPlain) return;
 
-  block_sum<NV>(part, smem);
+  // per-block totals, column-major over the lanes' slots = global column order
+  double bsum[NV];
+  block_sum_slots<NVL, CL>(part, smem, bsum);
   if (threadIdx.x == 0)
 #pragma unroll
-    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
   if (!last_block(ctl.counter)) return;
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
@@ -994,50 +1033,64 @@ __global__ void k_cpl_count(const int* __restrict__ nbr_off, const uint8_t* __re
   }
 }
 
+// Vector kernels: a thread owns CW = min(K, 2) adjacent right-hand sides of
+// one row (32 contiguous bytes per vector: a warp touches 1 KB runs), KH =
+// K / CW threads share a row; the thread's column slot h = lane % KH is fixed
+// because the grid stride is a multiple of KH.
+template <int K>
+struct VecMap {
+  static constexpr int CW = K >= 2 ? 2 : 1;
+  static constexpr int KH = K / CW;
+};
+
 // x += alpha p ; r -= alpha q ; z = D^-1 r ; partial r^T z, ||r||^2
 // last block: convergence test, beta, rho.
 template <int K>
 __global__ void __launch_bounds__(kBlock)
 k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const double2* __restrict__ p,
          const double2* __restrict__ q, const double2* __restrict__ dinv, KrylovCtl ctl) {
-  constexpr int NV = 3 * K;
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
+  constexpr int NVL = 3 * CW, NV = 3 * K;
   __shared__ double smem[32 * NV];
   if (*ctl.n_active == 0) return;
-  bool act[K];
-  double2 alpha[K];
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  bool act[CW];
+  double2 alpha[CW];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    act[k] = ctl.st[k].status == kActive;
-    alpha[k] = ctl.st[k].alpha;
+  for (int c = 0; c < CW; ++c) {
+    act[c] = ctl.st[kb + c].status == kActive;
+    alpha[c] = ctl.st[kb + c].alpha;
   }
-  double part[NV];
+  double part[NVL];
 #pragma unroll
-  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
   const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows;
-       j += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
     const double2 d = dinv[i];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (!act[k]) continue;
-      const int64_t idx = i * K + k;
+    for (int c = 0; c < CW; ++c) {
+      if (!act[c]) continue;
+      const int64_t idx = i * K + kb + c;
       const double2 pv = p[idx], qv = q[idx];
       double2 xv = x[idx], rv = r[idx];
-      xv = cadd(xv, cmul(alpha[k], pv));
-      rv = csub(rv, cmul(alpha[k], qv));
+      xv = cadd(xv, cmul(alpha[c], pv));
+      rv = csub(rv, cmul(alpha[c], qv));
       x[idx] = xv;
       r[idx] = rv;
       const double2 z = cmul(d, rv);
-      part[3 * k] += rv.x * z.x - rv.y * z.y;
-      part[3 * k + 1] += rv.x * z.y + rv.y * z.x;
-      part[3 * k + 2] += rv.x * rv.x + rv.y * rv.y;
+      part[3 * c] += rv.x * z.x - rv.y * z.y;
+      part[3 * c + 1] += rv.x * z.y + rv.y * z.x;
+      part[3 * c + 2] += rv.x * rv.x + rv.y * rv.y;
     }
   }
-  block_sum<NV>(part, smem);
+  double bsum[NV];
+  block_sum_slots<NVL, KH>(part, smem, bsum);
   if (threadIdx.x == 0)
 #pragma unroll
-    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
   if (!last_block(ctl.counter)) return;
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
@@ -1057,24 +1110,27 @@ template <int K>
 __global__ void __launch_bounds__(kBlock)
 k_pupdate(int64_t n, const double2* __restrict__ r, double2* __restrict__ p,
           const double2* __restrict__ dinv, KrylovCtl ctl) {
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
   if (*ctl.n_active == 0) return;
-  bool act[K];
-  double2 beta[K];
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  bool act[CW];
+  double2 beta[CW];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    act[k] = ctl.st[k].status == kActive;
-    beta[k] = ctl.st[k].beta;
+  for (int c = 0; c < CW; ++c) {
+    act[c] = ctl.st[kb + c].status == kActive;
+    beta[c] = ctl.st[kb + c].beta;
   }
   const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows;
-       j += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
     const double2 d = dinv[i];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (!act[k]) continue;
-      const int64_t idx = i * K + k;
-      p[idx] = cadd(cmul(d, r[idx]), cmul(beta[k], p[idx]));
+    for (int c = 0; c < CW; ++c) {
+      if (!act[c]) continue;
+      const int64_t idx = i * K + kb + c;
+      p[idx] = cadd(cmul(d, r[idx]), cmul(beta[c], p[idx]));
     }
   }
 }
@@ -1087,40 +1143,44 @@ __global__ void __launch_bounds__(kBlock)
 k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, double2* __restrict__ r,
         double2* __restrict__ p, const double2* __restrict__ dinv, unsigned mask, int fresh,
         KrylovCtl ctl) {
-  constexpr int NV = 4 * K;
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
+  constexpr int NVL = 4 * CW, NV = 4 * K;
   __shared__ double smem[32 * NV];
-  double part[NV];
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  double part[NVL];
 #pragma unroll
-  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
   const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows;
-       j += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
     const double2 d = dinv[i];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (!((mask >> k) & 1u)) continue;
-      const int64_t idx = i * K + k;
+    for (int c = 0; c < CW; ++c) {
+      if (!((mask >> (kb + c)) & 1u)) continue;
+      const int64_t idx = i * K + kb + c;
       double2 rv;
       if (fresh) {
         rv = b[idx];
         x[idx] = make_double2(0.0, 0.0);
         r[idx] = rv;
-        part[4 * k + 3] += rv.x * rv.x + rv.y * rv.y;
+        part[4 * c + 3] += rv.x * rv.x + rv.y * rv.y;
       } else {
         rv = r[idx];
       }
       const double2 z = cmul(d, rv);
       p[idx] = z;
-      part[4 * k] += rv.x * z.x - rv.y * z.y;
-      part[4 * k + 1] += rv.x * z.y + rv.y * z.x;
-      part[4 * k + 2] += rv.x * rv.x + rv.y * rv.y;
+      part[4 * c] += rv.x * z.x - rv.y * z.y;
+      part[4 * c + 1] += rv.x * z.y + rv.y * z.x;
+      part[4 * c + 2] += rv.x * rv.x + rv.y * rv.y;
     }
   }
-  block_sum<NV>(part, smem);
+  double bsum[NV];
+  block_sum_slots<NVL, KH>(part, smem, bsum);
   if (threadIdx.x == 0)
 #pragma unroll
-    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
   if (!last_block(ctl.counter)) return;
   double tot[NV];
   reduce_partials<NV>(ctl.partial, tot, smem);
@@ -1190,26 +1250,34 @@ const void* nbt_fn() {
 // (ECT_NB_VARIANT, read at context creation; 0 is the default).
 template <int K>
 const void* nb_fn(int variant, int mode) {
-#define ECT_NBF(G_, MB_)                                                   \
-  (mode == kPlain  ? (const void*)k_nb_spmv<G_, K, kPlain, MB_>            \
-   : mode == kCocg ? (const void*)k_nb_spmv<G_, K, kCocg, MB_>             \
-                   : (const void*)k_nb_spmv<G_, K, kResid, MB_>)
-  if constexpr (K <= 4) {
+#define ECT_NBF(G_, MB_, CL_)                                                   \
+  (mode == kPlain  ? (const void*)k_nb_spmv<G_, K, kPlain, MB_, CL_>            \
+   : mode == kCocg ? (const void*)k_nb_spmv<G_, K, kCocg, MB_, CL_>             \
+                   : (const void*)k_nb_spmv<G_, K, kResid, MB_, CL_>)
+  // Measured on B200 (configs[1]): 2 block lanes per node with <= 2
+  // right-hand sides per lane (column lanes for wider batches), 2 CTAs/SM.
+  if constexpr (K <= 2) {
     switch (variant) {
-      case 1: return ECT_NBF(4, 1);
-      case 4: return ECT_NBF(8, 2);
-      case 6: return ECT_NBF(8, 1);
-      case 7: return ECT_NBF(2, 2);
-      case 9: return ECT_NBF(1, 2);
-      case 8: return ECT_NBF(2, 1);
-      case 10: return ECT_NBF(4, 2);
-      case 11: return ECT_NBF(2, 3);
-      case 12: return ECT_NBF(4, 3);
-      case 13: return ECT_NBF(2, 4);
-      default: return ECT_NBF(2, 2);  // measured best on B200 (configs[1], k = 1, 2, 4)
+      case 1: return ECT_NBF(4, 1, 1);
+      case 4: return ECT_NBF(8, 2, 1);
+      case 9: return ECT_NBF(1, 2, 1);
+      default: return ECT_NBF(2, 2, 1);
     }
+  } else if constexpr (K == 4) {
+    switch (variant) {
+      case 7: return ECT_NBF(2, 2, 1);   // 2 block lanes x 4 columns (spills)
+      case 15: return ECT_NBF(4, 2, 2);  // 2 block lanes x 2 column lanes
+      default: return ECT_NBF(2, 2, 2);  // 1 block lane x 2 column lanes
+    }
+  } else if constexpr (K == 8) {
+    switch (variant) {
+      case 16: return ECT_NBF(8, 1, 1);
+      case 17: return ECT_NBF(8, 2, 4);  // 2 block lanes x 4 column lanes
+      default: return ECT_NBF(4, 2, 4);  // 1 block lane x 4 column lanes
+    }
+  } else {
+    return ECT_NBF(8, 2, 8);
   }
-  return ECT_NBF(8, 1);
 #undef ECT_NBF
 }
 
