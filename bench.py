@@ -390,7 +390,8 @@ def run_reference(args):
 
 def run_micro(args):
     """configs[2]: 200 fixed Krylov iterations on the assembled configs[1]
-    matrix, right-hand side re/im uniform [-1, 1] from seed 2, CSR vs NB."""
+    matrix, right-hand side re/im uniform [-1, 1] from seed 2: CSR vs SELL-32-sigma
+    (the storage pair configs[2] names) vs the node-block format (NB)."""
     import torch
     from paper_1602_03207_b200 import ect, workloads
     w = workloads.config1()
@@ -400,7 +401,7 @@ def run_micro(args):
     p, _, _ = mesh.materials(w.physics)
     rng = np.random.default_rng(2)
     out = {}
-    for fmt in ("nb", "csr"):
+    for fmt in ("nb", "sell", "csr"):
         ctx.set_format(fmt)
         a = ect.Matrix(ctx, mesh).assemble(p)
         n = a.n

@@ -142,8 +142,9 @@ int ect_ctx_synchronize(ect_ctx* ctx);
 #define ECT_FORMAT_NB 0
 #define ECT_FORMAT_CSR 1
 #define ECT_FORMAT_NB_TILED 2 /* NB + shared-memory x tiles (measured slower on B200) */
+#define ECT_FORMAT_SELL 3     /* SELL-32-sigma (sigma = 256), configs[2]'s comparison */
 int ect_ctx_set_format(ect_ctx* ctx, int format);
-/* 0: CSR, 1: NB untiled, 2: NB with shared-memory x tiles. */
+/* 0: CSR, 1: NB untiled, 2: NB with shared-memory x tiles, 3: SELL-C-sigma. */
 int ect_matrix_format(ect_matrix* m, int32_t* nb);
 /* NB storage counts: 3x3 node blocks and conductor couplings (0 for CSR). */
 int ect_matrix_nb_counts(ect_matrix* m, int64_t* blocks, int64_t* couplings);

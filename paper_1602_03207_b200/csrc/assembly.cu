@@ -259,7 +259,8 @@ void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a) {
   if (h_err) fail(ECT_ERR_MESH, "element frame on a degenerate or inverted tet");
   a->assembled = true;
   compute_jacobi(a);
-  if (!ctx->force_csr) build_nb(m, a);
+  if (ctx->use_sell) build_sell(a, ctx->sell_sigma);
+  else if (!ctx->force_csr) build_nb(m, a);
 }
 
 }  // namespace ect

@@ -101,6 +101,9 @@ struct ect_ctx {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
   bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
+  bool use_sell = false;                        // ect_ctx_set_format(ctx, ECT_FORMAT_SELL)
+  bool use_nbe = true;                          // NB-E sliced-ELL blocks (default; variants 1..49 off)
+  int sell_sigma = 256;
   struct SolverWorkspace {                      // cocg_solve buffers, reused across solves
     ect::DevBuf<double2> bb, xx, r, p, q;
     ect::DevBuf<ect::RhsState> st;
@@ -151,6 +154,7 @@ struct ect_matrix {
   // 6 double2 planes) over the neighbour list, and conductor couplings
   // (A-V column, V-A row, V-V entry: 4 double2 planes).
   bool has_nb = false;
+  int nbs_cap[3] = {-1, -1, -1};    // staged SpMV ring-slot blocks for 4 / 8 / 16 nodes per warp
   int64_t nb_blocks = 0, nb_ncpl = 0;
   const int* nb_blk_ptr = nullptr;  // = mesh->nbr_off (borrowed)
   const int* nb_blk_col = nullptr;  // = mesh->nbr (borrowed)
@@ -159,6 +163,16 @@ struct ect_matrix {
   ect::DevBuf<int> nb_cpl_ptr;      // n_nodes + 1
   ect::DevBuf<int2> nb_cpl_idx;     // (node m, cond dof of m)
   ect::DevBuf<double2> nb_cpl;      // [4][nb_cpl]
+  // NB-E: sliced-ELL copy of the NB blocks (chunks of 32 nodes, slot-major)
+  bool has_nbe = false;
+  int64_t nbe_slots = 0;
+  ect::DevBuf<int> nbe_off, nbe_col;
+  ect::DevBuf<double2> nbe_blk;
+  // SELL-C-sigma (ECT_FORMAT_SELL): chunk offsets, slot -> row, padded entries
+  bool has_sell = false;
+  int64_t sell_chunks = 0, sell_stored = 0;
+  ect::DevBuf<int> sell_off, sell_perm, sell_col;
+  ect::DevBuf<double2> sell_val;
   // NB-T: tiles of consecutive nodes with a staged x footprint
   bool has_nbt = false;
   int64_t nbt_tiles = 0;
@@ -204,6 +218,7 @@ void export_csc_values(ect_matrix* a, double2* out);           // pattern.cu (sy
 void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a);  // assembly.cu
 void compute_jacobi(ect_matrix* a);                            // krylov.cu
 void build_nb(ect_mesh* m, ect_matrix* a);                     // krylov.cu (NB format)
+void build_sell(ect_matrix* a, int sigma);                     // krylov.cu (SELL-C-sigma)
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k);  // spmv.cu
 void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* which, int n_rhs,
                double amplitude, double2* rhs);                // rhs.cu

@@ -193,6 +193,9 @@ int ect_ctx_create(int device, ect_ctx** out) {
     }
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* v = std::getenv("ECT_NB_VARIANT")) ctx->nb_variant = std::atoi(v);
+    // NB-E (sliced-ELL blocks) is the default SpMV layout; variants 1..49 select
+    // the per-node NB kernels it was measured against
+    ctx->use_nbe = ctx->nb_variant == 0 || ctx->nb_variant >= 50;
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev_a));
     CK(cudaEventCreate(&ctx->ev_b));
@@ -236,16 +239,17 @@ int ect_ctx_set_profiling(ect_ctx* ctx, int enabled) {
 int ect_ctx_set_format(ect_ctx* ctx, int format) {
   return guarded([&] {
     require(format == ECT_FORMAT_NB || format == ECT_FORMAT_CSR ||
-                format == ECT_FORMAT_NB_TILED,
+                format == ECT_FORMAT_NB_TILED || format == ECT_FORMAT_SELL,
             ECT_ERR_CONFIG, "ect_ctx_set_format: unknown format");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
-    ctx->force_csr = format == ECT_FORMAT_CSR;
+    ctx->force_csr = format == ECT_FORMAT_CSR || format == ECT_FORMAT_SELL;
+    ctx->use_sell = format == ECT_FORMAT_SELL;
     ctx->no_tiles = format != ECT_FORMAT_NB_TILED;
   });
 }
 
 int ect_matrix_format(ect_matrix* m, int32_t* nb) {
-  return guarded([&] { *nb = m->has_nb ? (m->has_nbt ? 2 : 1) : 0; });
+  return guarded([&] { *nb = m->has_nb ? (m->has_nbt ? 2 : 1) : (m->has_sell ? 3 : 0); });
 }
 
 int ect_matrix_nb_counts(ect_matrix* m, int64_t* blocks, int64_t* couplings) {
@@ -478,6 +482,7 @@ int ect_matrix_from_csr(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* row
     CK(cudaStreamSynchronize(ctx->stream));
     a->assembled = true;
     ect::compute_jacobi(a.get());
+    if (ctx->use_sell) ect::build_sell(a.get(), ctx->sell_sigma);
     *out = a.release();
   });
 }

@@ -385,6 +385,7 @@ struct NbView {
   const int* cond_fwd;
   int64_t n_nodes;  // nodes whose rows this view computes (owned nodes)
   int64_t na;       // V block offset in the x/y layout (3 n_nodes, or 3 (L + G) on a part)
+  const int* e_off = nullptr;  // NB-E: chunk slot offsets (blk / blk_col are then slot-major)
 };
 
 // 256-bit streaming load (read-once matrix data: no L1 allocation)
@@ -438,6 +439,136 @@ __device__ __forceinline__ int2 ldg_i2(const int2* p) {
   int2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
   return v;
+}
+
+// ---- SELL-C-sigma SpMV (configs[2]'s storage comparison) -------------------------
+// Rows sorted by length (descending) inside windows of sigma rows, then cut
+// into chunks of C = 32 rows (one warp); a chunk stores its entries column-
+// major and padded to the chunk's widest row, so entry j of the 32 rows is one
+// contiguous 512-byte (values) + 128-byte (columns) access. Same 20 B per
+// stored entry as CSR plus padding; slot -> row permutation applied on write.
+constexpr int kSellC = 32;
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_sell_spmv(int64_t n_chunks, const int* __restrict__ off, const int* __restrict__ perm,
+            const int* __restrict__ scol, const double2* __restrict__ sval,
+            const double2* __restrict__ x, double2* __restrict__ y, const double2* __restrict__ b,
+            KrylovCtl ctl) {
+  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
+  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  bool act[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) act[k] = (MODE == kPlain) || ctl.st[k].status == kActive;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) part[j] = 0.0;
+  for (int64_t c = warp; c < n_chunks; c += n_warps) {
+    const int o0 = off[c], w = (off[c + 1] - o0) / kSellC;
+    const int row = perm[c * kSellC + lane];
+    double2 acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int j = 0; j < w; ++j) {
+      const int e = o0 + j * kSellC + lane;
+      const int jc = ldg_i(scol + e);
+      const double2 a = ldg2(sval + e);
+      double2 xv[K];
+      load_xk<K>(x + (int64_t)jc * K, xv);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        acc[k].x += a.x * xv[k].x - a.y * xv[k].y;
+        acc[k].y += a.x * xv[k].y + a.y * xv[k].x;
+      }
+    }
+    if (row >= 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        const int64_t idx = (int64_t)row * K + k;
+        if (MODE == kPlain) {
+          y[idx] = acc[k];
+        } else if (MODE == kCocg) {
+          y[idx] = acc[k];
+          const double2 pv = x[idx];
+          part[2 * k] += pv.x * acc[k].x - pv.y * acc[k].y;
+          part[2 * k + 1] += pv.x * acc[k].y + pv.y * acc[k].x;
+        } else {
+          const double2 rv = csub(b[idx], acc[k]);
+          y[idx] = rv;
+          part[k] += rv.x * rv.x + rv.y * rv.y;
+        }
+      }
+    }
+  }
+  if (MODE == kPlain) return;
+  block_sum<NV>(part, smem);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    if (ctl.red) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
+    } else {
+      fin_resid<K>(ctl, tot);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
+__global__ void k_sell_lens(int64_t n, const int* __restrict__ row_ptr, int* __restrict__ len,
+                            int* __restrict__ idx, int64_t n_pad) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_pad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    len[r] = r < n ? row_ptr[r + 1] - row_ptr[r] : 0;
+    idx[r] = r < n ? (int)r : -1;
+  }
+}
+
+// chunk width = longest row of the chunk (rows are sorted inside sigma windows)
+__global__ void k_sell_width(int64_t n_chunks, const int* __restrict__ slen, int* __restrict__ w) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int m = 0;
+    for (int l = 0; l < kSellC; ++l) m = max(m, slen[c * kSellC + l]);
+    w[c] = kSellC * m;
+  }
+}
+
+__global__ void k_sell_fill(int64_t n_slots, const int* __restrict__ perm,
+                            const int* __restrict__ off, const int* __restrict__ row_ptr,
+                            const int* __restrict__ col, const double2* __restrict__ val,
+                            int* __restrict__ scol, double2* __restrict__ sval) {
+  for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < n_slots;
+       sl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = sl / kSellC;
+    const int lane = (int)(sl % kSellC);
+    const int o0 = off[c], w = (off[c + 1] - o0) / kSellC;
+    const int r = perm[sl];
+    const int beg = r >= 0 ? row_ptr[r] : 0, len = r >= 0 ? row_ptr[r + 1] - beg : 0;
+    const int pad_col = len > 0 ? col[beg + len - 1] : 0;
+    for (int j = 0; j < w; ++j) {
+      const int64_t e = o0 + (int64_t)j * kSellC + lane;
+      if (j < len) {
+        scol[e] = col[beg + j];
+        sval[e] = val[beg + j];
+      } else {
+        scol[e] = pad_col;  // stays in the row's own x neighbourhood
+        sval[e] = make_double2(0.0, 0.0);
+      }
+    }
+  }
 }
 
 // G lanes per node = GB block lanes x CL column lanes. Block lane bl streams
@@ -660,6 +791,517 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
     }
     *ctl.counter = 0u;
   }
+}
+
+// Same kernel over the sliced-ELL block layout (NB-E): chunks of 32 nodes,
+// block j of the chunk's nodes stored contiguously (1 KB per plane), padded to
+// the chunk's largest degree with zero blocks. A warp's block loads become
+// contiguous runs instead of 16-32 scattered 64-byte pieces.
+template <int G, int K, int MODE, int MINB, int CL>
+__global__ void __launch_bounds__(kBlock, MINB)
+k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
+          const double2* __restrict__ b, KrylovCtl ctl) {
+  static_assert(G % CL == 0 && K % CL == 0, "lane split");
+  constexpr int GB = G / CL;   // block lanes per node
+  constexpr int KL = K / CL;   // right-hand sides per lane
+  constexpr int NVL = (MODE == kCocg) ? 2 * KL : (MODE == kResid ? KL : 1);  // per lane
+  constexpr int NV = NVL * CL;
+  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  constexpr int NPW = 32 / G;  // nodes per warp and pass
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const int bl = g / CL, cl = g % CL;
+  const int kc = cl * KL;      // first column of this lane
+  bool act[KL];
+#pragma unroll
+  for (int k = 0; k < KL; ++k) act[k] = (MODE == kPlain) || ctl.st[kc + k].status == kActive;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t na = A.na;
+  double part[NVL];  // this lane's columns [kc, kc + KL)
+#pragma unroll
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
+
+  for (int64_t wn = warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
+    const int64_t i = wn + lane / G;
+    const bool valid = i < A.n_nodes;
+    double2 acc[3][KL], accv[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+      acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
+    }
+    int cf_i = -1;
+    if (valid) {
+      // sliced-ELL blocks: block j of node i at slot off[c] + 32 j + (i mod 32)
+      const int c32 = (int)(i >> 5);
+      const int o32 = A.e_off[c32];
+      const int w32 = (A.e_off[c32 + 1] - o32) >> 5;
+      const int sbase = o32 + (int)(i & 31);
+      const int be = sbase + 32 * w32;
+      constexpr int GS = 32 * GB;  // slot stride between a lane's blocks
+      int q = sbase + 32 * bl;
+      int m_nx = 0;
+      double B_nx[3][3], Im_nx[3];
+      if (q < be) {
+        m_nx = ldg_i(A.blk_col + q);
+        load_block(A, q, B_nx, Im_nx);
+      }
+      // (wide per-lane batches keep the accumulators instead)
+      constexpr bool kPipe = KL <= 2 && MINB <= 2;
+      for (; q < be; q += GS) {
+        int m = m_nx;
+        double B[3][3], Im[3];
+        if constexpr (kPipe) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            Im[c] = Im_nx[c];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
+          }
+          if (q + GS < be) {
+            m_nx = ldg_i(A.blk_col + q + GS);
+            load_block(A, q + GS, B_nx, Im_nx);
+          }
+        } else {
+          if (q != sbase + 32 * bl) {
+            m = ldg_i(A.blk_col + q);
+            load_block(A, q, B, Im);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              Im[c] = Im_nx[c];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
+            }
+          }
+        }
+        const double2* xm = x + (int64_t)3 * m * K + kc;
+        // right-hand sides in pairs: one 256-bit gather per (component, pair)
+        constexpr int KP = (KL % 2 == 0) ? 2 : 1;
+#pragma unroll
+        for (int k0 = 0; k0 < KL; k0 += KP) {
+          if (!act[k0] && !act[k0 + KP - 1]) continue;
+          double2 xp[3][KP];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if constexpr (KP == 2) ld4x(xm + d * K + k0, xp[d][0], xp[d][1]);
+            else xp[d][0] = __ldg(xm + d * K + k0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) {
+            const int k = k0 + kk;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double2 s = acc[c][k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                s.x += B[c][d] * xp[d][kk].x;
+                s.y += B[c][d] * xp[d][kk].y;
+              }
+              s.x -= Im[c] * xp[c][kk].y;
+              s.y += Im[c] * xp[c][kk].x;
+              acc[c][k] = s;
+            }
+          }
+        }
+      }
+      cf_i = A.cond_fwd[i];
+      if (cf_i >= 0) {
+        const int ce = A.cpl_ptr[i + 1];
+        for (int q = A.cpl_ptr[i] + bl; q < ce; q += GB) {
+          const int2 mi = ldg_i2(A.cpl_idx + q);
+          double av[3], va[3];
+          double2 Q3;
+          load_cpl(A, q, av, va, Q3);
+          const double2* xm = x + (int64_t)3 * mi.x * K + kc;
+          const double2* xvp = x + (na + mi.y) * K + kc;
+          constexpr int KP = (KL % 2 == 0) ? 2 : 1;
+#pragma unroll
+          for (int k0 = 0; k0 < KL; k0 += KP) {
+            if (!act[k0] && !act[k0 + KP - 1]) continue;
+            double2 xa[3][KP], xv[KP];
+            if constexpr (KP == 2) {
+              ld4x(xvp + k0, xv[0], xv[1]);
+#pragma unroll
+              for (int d = 0; d < 3; ++d) ld4x(xm + d * K + k0, xa[d][0], xa[d][1]);
+            } else {
+              xv[0] = __ldg(xvp + k0);
+#pragma unroll
+              for (int d = 0; d < 3; ++d) xa[d][0] = __ldg(xm + d * K + k0);
+            }
+#pragma unroll
+            for (int kk = 0; kk < KP; ++kk) {
+              const int k = k0 + kk;
+              const double2 v = xv[kk];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                acc[c][k].x += av[c] * v.x;
+                acc[c][k].y += av[c] * v.y;
+              }
+              double2 s = accv[k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                s.x += va[d] * xa[d][kk].x;
+                s.y += va[d] * xa[d][kk].y;
+              }
+              s.x += Q3.x * v.x - Q3.y * v.y;
+              s.y += Q3.x * v.y + Q3.y * v.x;
+              accv[k] = s;
+            }
+          }
+        }
+      }
+    }
+    // segment reduction over the GB block lanes of a node (same column lane)
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+#pragma unroll
+      for (int o = (GB / 2) * CL; o >= CL; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
+          acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
+        }
+        accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
+        accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
+      }
+    }
+    if (bl == 0 && valid) {
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+        if (!act[k]) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c == 3 && cf_i < 0) break;
+          const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
+          const double2 v = c < 3 ? acc[c][k] : accv[k];
+          const int64_t idx = row * K + kc + k;
+          if (MODE == kPlain) {
+            y[idx] = v;
+          } else if (MODE == kCocg) {
+            y[idx] = v;
+            const double2 pv = x[idx];
+            part[2 * k] += pv.x * v.x - pv.y * v.y;
+            part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
+          } else {
+            const double2 rv = csub(b[idx], v);
+            y[idx] = rv;
+            part[k] += rv.x * rv.x + rv.y * rv.y;
+          }
+        }
+      }
+    }
+  }
+  if (MODE == kPlain) return;
+
+  // per-block totals, column-major over the lanes' slots = global column order
+  double bsum[NV];
+  block_sum_slots<NVL, CL>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    if (ctl.red) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
+    } else {
+      fin_resid<K>(ctl, tot);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
+// ---- staged NB SpMV (NB-S): TMA bulk copies of the matrix stream -------------
+// The NB matrix stream of a group of NPW = 32 / G consecutive nodes is one
+// contiguous range of blocks [q0, q1) in each plane, so one elected lane per
+// warp moves it into a shared-memory ring slot with four cp.async.bulk copies
+// (3 planes + column indices) completing on an mbarrier, a group ahead of the
+// compute. The lanes then read their 3x3 blocks from shared memory; their
+// registers hold the x gathers one block ahead instead of in-flight matrix
+// loads (the register-pipelined kernel's limit for wide batches).
+constexpr int kSlots = 2;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n"
+      "DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// bytes of one ring slot for `cap` blocks (planes + columns), 128-B multiple
+__host__ __device__ inline size_t nbs_slot_bytes(int cap) {
+  return ((size_t)100 * cap + 127) & ~(size_t)127;
+}
+template <int NV, int NWARP>
+size_t nbs_smem(int cap) {
+  return (size_t)NWARP * kSlots * nbs_slot_bytes(cap) + NWARP * kSlots * sizeof(uint64_t) +
+         32 * NV * sizeof(double);
+}
+
+template <int G, int K, int MODE, int CL, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32, 1)
+k_nbs_spmv(NbView A, int cap, const double2* __restrict__ x, double2* __restrict__ y,
+           const double2* __restrict__ b, KrylovCtl ctl) {
+  static_assert(G % CL == 0 && K % CL == 0, "lane split");
+  constexpr int GB = G / CL;
+  constexpr int KL = K / CL;
+  constexpr int NVL = (MODE == kCocg) ? 2 * KL : (MODE == kResid ? KL : 1);
+  constexpr int NV = NVL * CL;
+  constexpr int NPW = 32 / G;
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane & (G - 1);
+  const int bl = g / CL, cl = g % CL;
+  const int kc = cl * KL;
+  const size_t slot_bytes = nbs_slot_bytes(cap);
+  unsigned char* ring = sm_raw + (size_t)wid * kSlots * slot_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + (size_t)NWARP * kSlots * slot_bytes) +
+                   wid * kSlots;
+  double* red = reinterpret_cast<double*>(bars - wid * kSlots + NWARP * kSlots);
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  bool act[KL];
+#pragma unroll
+  for (int k = 0; k < KL; ++k) act[k] = (MODE == kPlain) || ctl.st[kc + k].status == kActive;
+  const int64_t na = A.na;
+  const int64_t n_groups = (A.n_nodes + NPW - 1) / NPW;
+  const int64_t gstride = (int64_t)gridDim.x * NWARP;
+  double part[NVL];
+#pragma unroll
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
+
+  auto issue = [&](int64_t grp, int s) {
+    if (lane == 0) {
+      const int64_t n0 = grp * NPW;
+      const int64_t n1 = n0 + NPW < A.n_nodes ? n0 + NPW : A.n_nodes;
+      const int qa = A.blk_ptr[n0] & ~3, qb = (A.blk_ptr[n1] + 3) & ~3;
+      const int nq = qb - qa;
+      unsigned char* slot = ring + (size_t)s * slot_bytes;
+      mbar_expect_tx(&bars[s], 100u * nq);
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        bulk_g2s(slot + (size_t)p * cap * 32, A.blk + 4 * ((int64_t)p * A.nblk + qa), 32u * nq,
+                 &bars[s]);
+      bulk_g2s(slot + (size_t)3 * cap * 32, A.blk_col + qa, 4u * nq, &bars[s]);
+    }
+  };
+
+  unsigned phase = 0;
+  int s = 0;
+  int64_t grp = blockIdx.x * (int64_t)NWARP + wid;
+  if (grp < n_groups) issue(grp, 0);
+  for (; grp < n_groups; grp += gstride) {
+    __syncwarp();  // every lane is done with slot s ^ 1 (consumed last iteration)
+    if (grp + gstride < n_groups) issue(grp + gstride, s ^ 1);
+    mbar_wait(&bars[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const unsigned char* slot = ring + (size_t)s * slot_bytes;
+    const double* P0 = reinterpret_cast<const double*>(slot);
+    const double* P1 = P0 + 4 * cap;
+    const double* P2 = P0 + 8 * cap;
+    const int* col = reinterpret_cast<const int*>(slot + (size_t)3 * cap * 32);
+
+    const int64_t i = grp * NPW + lane / G;
+    const bool valid = i < A.n_nodes;
+    double2 acc[3][KL], accv[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
+    int cf_i = -1;
+    if (valid) {
+      const int qa = A.blk_ptr[grp * NPW] & ~3;
+      const int je = A.blk_ptr[i + 1] - qa;
+      int j = A.blk_ptr[i] - qa + bl;
+      double2 xc[3][KL];
+      if (j < je) {
+        const double2* xm = x + (int64_t)3 * col[j] * K + kc;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) load_xk<KL>(xm + d * K, xc[d]);
+      }
+      for (; j < je; j += GB) {
+        // gathers of the next block in flight while this block's FMAs run
+        double2 xn[3][KL];
+        if (j + GB < je) {
+          const double2* xm = x + (int64_t)3 * col[j + GB] * K + kc;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) load_xk<KL>(xm + d * K, xn[d]);
+        }
+        const double4 v0 = *reinterpret_cast<const double4*>(P0 + 4 * j);
+        const double4 v1 = *reinterpret_cast<const double4*>(P1 + 4 * j);
+        const double4 v2 = *reinterpret_cast<const double4*>(P2 + 4 * j);
+        const double B[3][3] = {{v0.x, v0.y, v0.z}, {v0.w, v1.x, v1.y}, {v1.z, v1.w, v2.x}};
+        const double Im[3] = {v2.y, v2.z, v2.w};
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double2 t = acc[c][k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              t.x += B[c][d] * xc[d][k].x;
+              t.y += B[c][d] * xc[d][k].y;
+            }
+            t.x -= Im[c] * xc[c][k].y;
+            t.y += Im[c] * xc[c][k].x;
+            acc[c][k] = t;
+          }
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int k = 0; k < KL; ++k) xc[d][k] = xn[d][k];
+      }
+      cf_i = A.cond_fwd[i];
+      if (cf_i >= 0) {
+        const int ce = A.cpl_ptr[i + 1];
+        for (int q = A.cpl_ptr[i] + bl; q < ce; q += GB) {
+          const int2 mi = ldg_i2(A.cpl_idx + q);
+          double av[3], va[3];
+          double2 Q3;
+          load_cpl(A, q, av, va, Q3);
+          const double2* xm = x + (int64_t)3 * mi.x * K + kc;
+          const double2* xvp = x + (na + mi.y) * K + kc;
+          constexpr int KP = KL % 2 == 0 ? 2 : 1;
+#pragma unroll
+          for (int k0 = 0; k0 < KL; k0 += KP) {
+            double2 xa[3][KP], xv[KP];
+            load_xk<KP>(xvp + k0, xv);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) load_xk<KP>(xm + d * K + k0, xa[d]);
+#pragma unroll
+            for (int kk = 0; kk < KP; ++kk) {
+              const int k = k0 + kk;
+              const double2 v = xv[kk];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                acc[c][k].x += av[c] * v.x;
+                acc[c][k].y += av[c] * v.y;
+              }
+              double2 t = accv[k];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                t.x += va[d] * xa[d][kk].x;
+                t.y += va[d] * xa[d][kk].y;
+              }
+              t.x += Q3.x * v.x - Q3.y * v.y;
+              t.y += Q3.x * v.y + Q3.y * v.x;
+              accv[k] = t;
+            }
+          }
+        }
+      }
+    }
+    s ^= 1;
+    // segment reduction over the GB block lanes of a node (same column lane)
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+#pragma unroll
+      for (int o = (GB / 2) * CL; o >= CL; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
+          acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
+        }
+        accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
+        accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
+      }
+    }
+    if (bl == 0 && valid) {
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+        if (!act[k]) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c == 3 && cf_i < 0) break;
+          const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
+          const double2 v = c < 3 ? acc[c][k] : accv[k];
+          const int64_t idx = row * K + kc + k;
+          if (MODE == kPlain) {
+            y[idx] = v;
+          } else if (MODE == kCocg) {
+            y[idx] = v;
+            const double2 pv = x[idx];
+            part[2 * k] += pv.x * v.x - pv.y * v.y;
+            part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
+          } else {
+            const double2 rv = csub(b[idx], v);
+            y[idx] = rv;
+            part[k] += rv.x * rv.x + rv.y * rv.y;
+          }
+        }
+      }
+    }
+  }
+  if (MODE == kPlain) return;
+
+  double bsum[NV];
+  block_sum_slots<NVL, CL>(part, red, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, red);
+  if (threadIdx.x == 0) {
+    if (ctl.red) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
+    } else {
+      fin_resid<K>(ctl, tot);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
+// max over node groups of the padded block count of one ring slot
+__global__ void k_nbs_cap(const int* __restrict__ blk_ptr, int64_t n_nodes, int npw,
+                          int* __restrict__ cap) {
+  const int64_t ng = (n_nodes + npw - 1) / npw;
+  int best = 0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = g * npw, n1 = n0 + npw < n_nodes ? n0 + npw : n_nodes;
+    const int nq = ((blk_ptr[n1] + 3) & ~3) - (blk_ptr[n0] & ~3);
+    best = nq > best ? nq : best;
+  }
+  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(cap, best);
 }
 
 // ---- tiled NB SpMV with shared-memory x staging (NB-T) -------------------------
@@ -1022,6 +1664,40 @@ __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __res
   }
 }
 
+// NB-E build: chunk widths (32 x the chunk's largest node degree) and the
+// slot-major copy of the NB planes / columns with zero padding blocks.
+__global__ void k_nbe_width(const int* __restrict__ blk_ptr, int64_t n_nodes, int64_t n_chunks,
+                            int* __restrict__ w) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_chunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int m = 0;
+    for (int64_t i = 32 * c; i < 32 * c + 32 && i < n_nodes; ++i) m = max(m, blk_ptr[i + 1] - blk_ptr[i]);
+    w[c] = 32 * m;
+  }
+}
+__global__ void k_nbe_fill(const int* __restrict__ blk_ptr, const int* __restrict__ blk_col,
+                           const double* __restrict__ blk, int64_t nblk, int64_t n_nodes,
+                           int64_t n_chunks, const int* __restrict__ off, int* __restrict__ ecol,
+                           double* __restrict__ eblk, int64_t nslots) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 32 * n_chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t >> 5, i = t;
+    const int l = (int)(t & 31);
+    const int o = off[c], w = (off[c + 1] - o) >> 5;
+    const int q0 = i < n_nodes ? blk_ptr[i] : 0, deg = i < n_nodes ? blk_ptr[i + 1] - q0 : 0;
+    for (int j = 0; j < w; ++j) {
+      const int64_t sl = o + 32 * (int64_t)j + l;
+      const bool real = j < deg;
+      ecol[sl] = real ? blk_col[q0 + j] : (i < n_nodes ? (int)i : 0);
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          eblk[4 * (pl * nslots + sl) + e] = real ? blk[4 * (pl * nblk + q0 + j) + e] : 0.0;
+    }
+  }
+}
+
 __global__ void k_cpl_count(const int* __restrict__ nbr_off, const uint8_t* __restrict__ nbr_cond,
                             const int* __restrict__ cond_fwd, int64_t n_nodes, int* cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
@@ -1228,7 +1904,6 @@ NbView nb_view(const ect_matrix* a) {
                 a->n_nodes, 3 * a->n_nodes};
 }
 
-constexpr int kNbG = 8;  // lanes per node in the NB SpMV
 constexpr size_t kNbtMaxSmem = 110 * 1024;
 
 NbtView nbt_view(const ect_matrix* a) {
@@ -1282,6 +1957,102 @@ const void* nb_fn(int variant, int mode) {
 }
 
 template <int K>
+const void* nbe_fn(int variant, int mode) {
+#define ECT_NBE(G_, MB_, CL_)                                                   \
+  (mode == kPlain  ? (const void*)k_nbe_spmv<G_, K, kPlain, MB_, CL_>            \
+   : mode == kCocg ? (const void*)k_nbe_spmv<G_, K, kCocg, MB_, CL_>             \
+                   : (const void*)k_nbe_spmv<G_, K, kResid, MB_, CL_>)
+  if constexpr (K <= 2) {
+    switch (variant) {
+      case 51: return ECT_NBE(4, 2, 1);
+      case 52: return ECT_NBE(1, 2, 1);
+      default: return ECT_NBE(2, 2, 1);
+    }
+  } else if constexpr (K == 4) {
+    switch (variant) {
+      case 51: return ECT_NBE(4, 2, 2);
+      case 52: return ECT_NBE(4, 2, 4);
+      default: return ECT_NBE(2, 2, 2);
+    }
+  } else if constexpr (K == 8) {
+    switch (variant) {
+      case 51: return ECT_NBE(8, 2, 4);
+      case 52: return ECT_NBE(8, 2, 8);
+      default: return ECT_NBE(4, 2, 4);
+    }
+  } else {
+    return ECT_NBE(8, 2, 8);
+  }
+#undef ECT_NBE
+}
+
+// Staged NB kernels (ECT_NB_VARIANT 30/31): function, warps per CTA, nodes per warp.
+struct NbsCfg {
+  const void* fn = nullptr;
+  int nwarp = 0, npw = 0;
+};
+template <int K>
+NbsCfg nbs_cfg(int variant, int mode) {
+#define ECT_NBS(G_, CL_, NW_)                                                              \
+  NbsCfg{mode == kPlain  ? (const void*)k_nbs_spmv<G_, K, kPlain, CL_, NW_>                \
+         : mode == kCocg ? (const void*)k_nbs_spmv<G_, K, kCocg, CL_, NW_>                 \
+                         : (const void*)k_nbs_spmv<G_, K, kResid, CL_, NW_>,               \
+         NW_, 32 / G_}
+  if (variant < 30 || variant > 33) return NbsCfg{};
+  if constexpr (K == 8) {
+    switch (variant) {
+      case 30: return ECT_NBS(4, 4, 8);
+      case 31: return ECT_NBS(8, 4, 16);
+      case 32: return ECT_NBS(8, 8, 16);
+      default: return ECT_NBS(8, 8, 8);
+    }
+  } else if constexpr (K == 4) {
+    switch (variant) {
+      case 30: return ECT_NBS(2, 2, 4);
+      case 31: return ECT_NBS(4, 2, 8);
+      case 32: return ECT_NBS(4, 4, 16);
+      default: return ECT_NBS(8, 4, 16);
+    }
+  } else if constexpr (K == 2) {
+    switch (variant) {
+      case 30: return ECT_NBS(2, 1, 4);
+      case 31: return ECT_NBS(4, 1, 8);
+      case 32: return ECT_NBS(4, 2, 8);
+      default: return ECT_NBS(8, 2, 16);
+    }
+  }
+  return NbsCfg{};
+#undef ECT_NBS
+}
+
+int nbs_cap(ect_matrix* a, int npw) {
+  const int slot = npw == 4 ? 0 : npw == 8 ? 1 : 2;
+  if (a->nbs_cap[slot] < 0) {
+    ect_ctx* ctx = a->ctx;
+    DevBuf<int> cap(1);
+    CK(cudaMemsetAsync(cap.p, 0, sizeof(int), ctx->stream));
+    k_nbs_cap<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(a->nb_blk_ptr, a->n_nodes, npw, cap.p);
+    CK_LAUNCH();
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, cap.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    a->nbs_cap[slot] = (h + 3) & ~3;
+  }
+  return a->nbs_cap[slot];
+}
+
+// dynamic shared memory of a staged launch (0: does not fit, use NB)
+template <int K>
+size_t nbs_bytes(const NbsCfg& c, ect_matrix* a, int mode) {
+  if (!c.fn || !a->has_nb) return 0;
+  const int cap = nbs_cap(a, c.npw);
+  const int cl_nv = mode == kCocg ? 2 * K : mode == kResid ? K : 1;
+  const size_t b = (size_t)c.nwarp * kSlots * nbs_slot_bytes(cap) +
+                   (size_t)c.nwarp * kSlots * sizeof(uint64_t) + 32 * (size_t)std::max(cl_nv, 8) * 8;
+  return b <= 227 * 1024 ? b : 0;
+}
+
+template <int K>
 struct Dispatch {
   static constexpr bool kNbOk = K <= 8;
   static constexpr bool kNbtOk = K <= 4;
@@ -1308,10 +2079,41 @@ struct Dispatch {
     if constexpr (kNbOk) {
       if (a->has_nb) {
         NbView v = nb_view(a);
+        const NbsCfg c = nbs_cfg<K>(ctx->nb_variant, mode);
+        if (const size_t sm = nbs_bytes<K>(c, const_cast<ect_matrix*>(a), mode)) {
+          int cap = nbs_cap(const_cast<ect_matrix*>(a), c.npw);
+          void* args[] = {&v, &cap, &x, &y, &b, &ctl};
+          CK(cudaLaunchKernel(c.fn, dim3(grid), dim3(32 * c.nwarp), args, sm, s));
+          return;
+        }
+        if (a->has_nbe) {
+          v.blk = reinterpret_cast<const double*>(a->nbe_blk.p);
+          v.blk_col = a->nbe_col.p;
+          v.nblk = a->nbe_slots;
+          v.e_off = a->nbe_off.p;
+          void* args[] = {&v, &x, &y, &b, &ctl};
+          CK(cudaLaunchKernel(nbe_fn<K>(ctx->nb_variant, mode), dim3(grid), dim3(kBlock), args, 0,
+                              s));
+          return;
+        }
         void* args[] = {&v, &x, &y, &b, &ctl};
         CK(cudaLaunchKernel(nb_fn<K>(ctx->nb_variant, mode), dim3(grid), dim3(kBlock), args, 0, s));
         return;
       }
+    }
+    if (a->has_sell) {
+      const int64_t nc = a->sell_chunks;
+      if (mode == kPlain)
+        k_sell_spmv<K, kPlain><<<grid, kBlock, 0, s>>>(nc, a->sell_off.p, a->sell_perm.p,
+                                                        a->sell_col.p, a->sell_val.p, x, y, b, ctl);
+      else if (mode == kCocg)
+        k_sell_spmv<K, kCocg><<<grid, kBlock, 0, s>>>(nc, a->sell_off.p, a->sell_perm.p,
+                                                       a->sell_col.p, a->sell_val.p, x, y, b, ctl);
+      else
+        k_sell_spmv<K, kResid><<<grid, kBlock, 0, s>>>(nc, a->sell_off.p, a->sell_perm.p,
+                                                        a->sell_col.p, a->sell_val.p, x, y, b, ctl);
+      CK_LAUNCH();
+      return;
     }
     constexpr int G = K >= 4 ? 8 : 16;
     if (mode == kPlain)
@@ -1349,7 +2151,21 @@ struct Dispatch {
       }
     }
     if constexpr (kNbOk) {
-      if (a->has_nb) return grid_for(ctx, nb_fn<K>(ctx->nb_variant, mode), kBlock);
+      if (a->has_nb) {
+        const NbsCfg c = nbs_cfg<K>(ctx->nb_variant, mode);
+        if (const size_t sm = nbs_bytes<K>(c, const_cast<ect_matrix*>(a), mode)) {
+          CK(cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          return ctx->num_sms;  // one CTA per SM (the ring fills shared memory)
+        }
+        if (a->has_nbe) return grid_for(ctx, nbe_fn<K>(ctx->nb_variant, mode), kBlock);
+        return grid_for(ctx, nb_fn<K>(ctx->nb_variant, mode), kBlock);
+      }
+    }
+    if (a->has_sell) {
+      const void* f = mode == kPlain  ? (const void*)k_sell_spmv<K, kPlain>
+                      : mode == kCocg ? (const void*)k_sell_spmv<K, kCocg>
+                                      : (const void*)k_sell_spmv<K, kResid>;
+      return grid_for(ctx, f, kBlock);
     }
     constexpr int G = K >= 4 ? 8 : 16;
     const void* f = mode == kPlain  ? (const void*)k_spmv<G, K, kPlain>
@@ -1462,7 +2278,8 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
   CK(cudaStreamSynchronize(s));
   a->nb_blocks = nblk;
   a->nb_ncpl = ncpl;
-  a->nb_blk.alloc(6 * std::max<int64_t>(1, nblk));
+  for (int& c : a->nbs_cap) c = -1;
+  a->nb_blk.alloc(6 * (std::max<int64_t>(1, nblk) + 4));  // + staged-copy overrun padding
   a->nb_cpl_idx.alloc(std::max(1, ncpl));
   a->nb_cpl.alloc(4 * (size_t)std::max(1, ncpl));
   a->nb_blk_ptr = m->nbr_off.p;
@@ -1489,6 +2306,33 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
     a->nb_cpl.release();
     a->nb_cpl_idx.release();
     return;
+  }
+  // ---- NB-E sliced-ELL copy of the blocks (chunks of 32 nodes) -----------------
+  a->has_nbe = false;
+  if (ctx->use_nbe) {
+    const int64_t nch = (nn + 31) / 32;
+    DevBuf<int> w(nch + 1);
+    const int cg = (int)std::min<int64_t>((nch + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_nbe_width<<<std::max(cg, 1), 256, 0, s>>>(m->nbr_off.p, nn, nch, w.p);
+    CK_LAUNCH();
+    a->nbe_off.alloc(nch + 1);
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, w.p, a->nbe_off.p, nch + 1, s));
+    CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, w.p, a->nbe_off.p, nch + 1, s));
+    int slots = 0;
+    CK(cudaMemcpyAsync(&slots, a->nbe_off.p + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    a->nbe_col.alloc(std::max(1, slots));
+    a->nbe_blk.alloc(6 * (size_t)std::max(1, slots));
+    const int fg = (int)std::min<int64_t>((32 * nch + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_nbe_fill<<<std::max(fg, 1), 256, 0, s>>>(m->nbr_off.p, m->nbr.p,
+                                                reinterpret_cast<const double*>(a->nb_blk.p), nblk,
+                                                nn, nch, a->nbe_off.p, a->nbe_col.p,
+                                                reinterpret_cast<double*>(a->nbe_blk.p), slots);
+    CK_LAUNCH();
+    note_launch(ctx, 2);
+    CK(cudaStreamSynchronize(s));
+    a->nbe_slots = slots;
+    a->has_nbe = true;
   }
   // ---- NB-T tile footprints --------------------------------------------------
   a->has_nbt = false;
@@ -1529,6 +2373,52 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
   a->nbt_tiles = ntiles;
   a->nbt_fmax = fmax;
   a->has_nbt = true;
+}
+
+void build_sell(ect_matrix* a, int sigma) {
+  ect_ctx* ctx = a->ctx;
+  cudaStream_t s = ctx->stream;
+  const int64_t n = a->n;
+  const int64_t n_chunks = (n + kSellC - 1) / kSellC, n_slots = n_chunks * kSellC;
+  sigma = std::max(kSellC, sigma / kSellC * kSellC);
+  DevBuf<int> len(n_slots), idx(n_slots), slen(n_slots), w(n_chunks + 1);
+  const int grid = (int)std::min<int64_t>((n_slots + 255) / 256, (int64_t)ctx->num_sms * 16);
+  k_sell_lens<<<std::max(grid, 1), 256, 0, s>>>(n, a->row_ptr.p, len.p, idx.p, n_slots);
+  CK_LAUNCH();
+  a->sell_perm.alloc(n_slots);
+  // sort rows by length (descending) inside windows of sigma rows
+  const int64_t n_win = (n_slots + sigma - 1) / sigma;
+  std::vector<int> h_seg(n_win + 1);
+  for (int64_t q = 0; q <= n_win; ++q) h_seg[q] = (int)std::min<int64_t>(q * sigma, n_slots);
+  DevBuf<int> seg(n_win + 1);
+  CK(cudaMemcpyAsync(seg.p, h_seg.data(), h_seg.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  size_t tmp = 0;
+  CK(cub::DeviceSegmentedSort::StableSortPairsDescending(nullptr, tmp, len.p, slen.p, idx.p,
+                                                         a->sell_perm.p, (int)n_slots, (int)n_win,
+                                                         seg.p, seg.p + 1, s));
+  CK(cub::DeviceSegmentedSort::StableSortPairsDescending(cub_scratch(ctx, tmp), tmp, len.p, slen.p,
+                                                         idx.p, a->sell_perm.p, (int)n_slots,
+                                                         (int)n_win, seg.p, seg.p + 1, s));
+  const int cgrid = (int)std::min<int64_t>((n_chunks + 255) / 256, (int64_t)ctx->num_sms * 16);
+  k_sell_width<<<std::max(cgrid, 1), 256, 0, s>>>(n_chunks, slen.p, w.p);
+  CK_LAUNCH();
+  a->sell_off.alloc(n_chunks + 1);
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, w.p, a->sell_off.p, n_chunks + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, w.p, a->sell_off.p, n_chunks + 1, s));
+  int total = 0;
+  CK(cudaMemcpyAsync(&total, a->sell_off.p + n_chunks, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  a->sell_col.alloc(std::max(1, total));
+  a->sell_val.alloc(std::max(1, total));
+  k_sell_fill<<<std::max(grid, 1), 256, 0, s>>>(n_slots, a->sell_perm.p, a->sell_off.p,
+                                                 a->row_ptr.p, a->col.p, a->val.p, a->sell_col.p,
+                                                 a->sell_val.p);
+  CK_LAUNCH();
+  note_launch(ctx, 4);
+  CK(cudaStreamSynchronize(s));
+  a->sell_chunks = n_chunks;
+  a->sell_stored = total;
+  a->has_sell = true;
 }
 
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {

@@ -228,7 +228,7 @@ static void build_neighbours(ect_mesh* m) {
     CK(cudaMemcpyAsync(&max_nbr, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }
-  m->nbr.alloc(std::max(1, total_nbr));
+  m->nbr.alloc(std::max(1, total_nbr) + 4);  // staged NB SpMV copies 16-B aligned ranges
   m->nbr_cond.alloc(std::max(1, total_nbr));
   k_write_neighbours<<<blocks_for(ctx, nn), 256, 0, s>>>(m->inc_off.p, cand_sorted.p,
                                                         m->nbr_off.p, nn, m->nbr.p,

@@ -152,7 +152,7 @@ class Context:
     def set_format(self, fmt: str):
         """SpMV storage of matrices assembled afterwards: 'nb' (default),
         'nb_tiled' (shared-memory x tiles) or 'csr'."""
-        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1, "nb_tiled": 2}[fmt])))
+        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1, "nb_tiled": 2, "sell": 3}[fmt])))
 
     def mark(self, slot: int):
         """Record event `slot` on the context stream (device-side timing)."""
@@ -253,7 +253,7 @@ class Matrix:
     def format(self) -> str:
         nb = I32()
         _check(lib().ect_matrix_format(self.h, C.byref(nb)))
-        return {0: "csr", 1: "nb", 2: "nb_tiled"}[nb.value]
+        return {0: "csr", 1: "nb", 2: "nb_tiled", 3: "sell"}[nb.value]
 
     def nb_stats(self) -> dict:
         b, c = I64(), I64()
