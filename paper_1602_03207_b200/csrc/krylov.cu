@@ -797,7 +797,7 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
 // block j of the chunk's nodes stored contiguously (1 KB per plane), padded to
 // the chunk's largest degree with zero blocks. A warp's block loads become
 // contiguous runs instead of 16-32 scattered 64-byte pieces.
-template <int G, int K, int MODE, int MINB, int CL>
+template <int G, int K, int MODE, int MINB, int CL, int PFD = 0>
 __global__ void __launch_bounds__(kBlock, MINB)
 k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           const double2* __restrict__ b, KrylovCtl ctl) {
@@ -850,6 +850,27 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       // (wide per-lane batches keep the accumulators instead)
       constexpr bool kPipe = KL <= 2 && MINB <= 2;
       for (; q < be; q += GS) {
+        if constexpr (PFD > 0) {
+          // L2 prefetch of the warp's block rows PFD steps ahead: the DRAM
+          // latency of the matrix stream is covered without holding registers
+          constexpr int LINES = NPW >= 4 ? NPW / 4 : 1;  // 128-B lines per plane row
+          const int row0 = (((q - sbase) >> 5) - bl + PFD * GB);
+          if (lane < 3 * LINES + 1) {
+#pragma unroll
+            for (int gb = 0; gb < GB; ++gb) {
+              const int jrow = row0 + gb;
+              if (jrow < w32) {
+                const int64_t wslot = o32 + (int)(wn & 31) + 32 * (int64_t)jrow;
+                const void* pa =
+                    lane < 3 * LINES
+                        ? (const void*)(A.blk + 4 * ((int64_t)(lane / LINES) * A.nblk + wslot) +
+                                        16 * (lane % LINES))
+                        : (const void*)(A.blk_col + wslot);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+              }
+            }
+          }
+        }
         int m = m_nx;
         double B[3][3], Im[3];
         if constexpr (kPipe) {
@@ -1962,28 +1983,42 @@ const void* nbe_fn(int variant, int mode) {
   (mode == kPlain  ? (const void*)k_nbe_spmv<G_, K, kPlain, MB_, CL_>            \
    : mode == kCocg ? (const void*)k_nbe_spmv<G_, K, kCocg, MB_, CL_>             \
                    : (const void*)k_nbe_spmv<G_, K, kResid, MB_, CL_>)
+#define ECT_NBEP(G_, MB_, CL_, PF_)                                             \
+  (mode == kPlain  ? (const void*)k_nbe_spmv<G_, K, kPlain, MB_, CL_, PF_>       \
+   : mode == kCocg ? (const void*)k_nbe_spmv<G_, K, kCocg, MB_, CL_, PF_>        \
+                   : (const void*)k_nbe_spmv<G_, K, kResid, MB_, CL_, PF_>)
   if constexpr (K <= 2) {
     switch (variant) {
       case 51: return ECT_NBE(4, 2, 1);
-      case 52: return ECT_NBE(1, 2, 1);
-      default: return ECT_NBE(2, 2, 1);
+      case 53: return ECT_NBEP(2, 2, 1, 2);
+      case 54: return ECT_NBEP(2, 2, 1, 4);
+      case 55: return ECT_NBEP(2, 2, 1, 8);
+      case 56: return ECT_NBE(2, 2, 1);
+      default: return ECT_NBEP(2, 2, 1, 2);  // measured best (configs[1], B200)
     }
   } else if constexpr (K == 4) {
     switch (variant) {
       case 51: return ECT_NBE(4, 2, 2);
-      case 52: return ECT_NBE(4, 2, 4);
-      default: return ECT_NBE(2, 2, 2);
+      case 53: return ECT_NBEP(2, 2, 2, 2);
+      case 54: return ECT_NBEP(2, 2, 2, 4);
+      case 55: return ECT_NBEP(2, 2, 2, 8);
+      case 56: return ECT_NBE(2, 2, 2);
+      default: return ECT_NBEP(2, 2, 2, 4);
     }
   } else if constexpr (K == 8) {
     switch (variant) {
       case 51: return ECT_NBE(8, 2, 4);
-      case 52: return ECT_NBE(8, 2, 8);
-      default: return ECT_NBE(4, 2, 4);
+      case 53: return ECT_NBEP(4, 2, 4, 2);
+      case 54: return ECT_NBEP(4, 2, 4, 4);
+      case 55: return ECT_NBEP(4, 2, 4, 8);
+      case 56: return ECT_NBE(4, 2, 4);
+      default: return ECT_NBEP(4, 2, 4, 4);
     }
   } else {
     return ECT_NBE(8, 2, 8);
   }
 #undef ECT_NBE
+#undef ECT_NBEP
 }
 
 // Staged NB kernels (ECT_NB_VARIANT 30/31): function, warps per CTA, nodes per warp.
