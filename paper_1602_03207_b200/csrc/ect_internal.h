@@ -192,6 +192,10 @@ struct ect_part {
   ect::DevBuf<int> blk_ptr, blk_col, cpl_ptr, cond_local;
   ect::DevBuf<int2> cpl_idx;
   ect::DevBuf<double2> blk, cpl, dinv;  // NB planes (3 x 4 doubles, 2 x 4 doubles), local dinv
+  bool has_nbe = false;                  // sliced-ELL copy of blk (default SpMV layout)
+  int64_t nbe_slots = 0;
+  ect::DevBuf<int> nbe_off, nbe_col;
+  ect::DevBuf<double2> nbe_blk;
   struct Peer {
     ect::DevBuf<int> send_nodes, send_cond;
     ect::DevBuf<double2> sendbuf;

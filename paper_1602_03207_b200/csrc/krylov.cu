@@ -2674,9 +2674,21 @@ __global__ void k_sum_parts(double* const* reds, int n_parts, int nv) {
 }
 
 NbView part_view(const ect_part* P) {
-  return NbView{P->blk_ptr.p, P->blk_col.p, reinterpret_cast<const double*>(P->blk.p), P->nblk,
-                P->cpl_ptr.p, P->cpl_idx.p, reinterpret_cast<const double*>(P->cpl.p), P->ncpl,
-                P->cond_local.p, P->plan.L, P->plan.na_local()};
+  NbView v{P->blk_ptr.p, P->blk_col.p, reinterpret_cast<const double*>(P->blk.p), P->nblk,
+           P->cpl_ptr.p, P->cpl_idx.p, reinterpret_cast<const double*>(P->cpl.p), P->ncpl,
+           P->cond_local.p, P->plan.L, P->plan.na_local()};
+  if (P->has_nbe) {  // sliced-ELL copy of the part's blocks (the default SpMV layout)
+    v.blk = reinterpret_cast<const double*>(P->nbe_blk.p);
+    v.blk_col = P->nbe_col.p;
+    v.nblk = P->nbe_slots;
+    v.e_off = P->nbe_off.p;
+  }
+  return v;
+}
+
+template <int K>
+const void* part_fn(const ect_part* P, int variant, int mode) {
+  return P->has_nbe ? nbe_fn<K>(variant, mode) : nb_fn<K>(variant, mode);
 }
 
 }  // namespace
@@ -2773,6 +2785,32 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
     if (d.nsc) CK(cudaMemcpy(d.send_cond.p, peer.send_cond_nodes.data(), d.nsc * sizeof(int), cudaMemcpyHostToDevice));
     P->peers.push_back(std::move(d));
   }
+  // NB-E copy of the part's blocks (same layout and kernels as a whole matrix)
+  if (ctx->use_nbe) {
+    const int64_t nch = (L + 31) / 32;
+    DevBuf<int> w(nch + 1);
+    const int cg = (int)std::min<int64_t>((nch + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_nbe_width<<<std::max(cg, 1), 256, 0, s>>>(P->blk_ptr.p, L, nch, w.p);
+    CK_LAUNCH();
+    P->nbe_off.alloc(nch + 1);
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, w.p, P->nbe_off.p, nch + 1, s));
+    CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, w.p, P->nbe_off.p, nch + 1, s));
+    int slots = 0;
+    CK(cudaMemcpyAsync(&slots, P->nbe_off.p + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    P->nbe_col.alloc(std::max(1, slots));
+    P->nbe_blk.alloc(6 * (size_t)std::max(1, slots));
+    const int fg = (int)std::min<int64_t>((32 * nch + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_nbe_fill<<<std::max(fg, 1), 256, 0, s>>>(P->blk_ptr.p, P->blk_col.p,
+                                                reinterpret_cast<const double*>(P->blk.p), P->nblk,
+                                                L, nch, P->nbe_off.p, P->nbe_col.p,
+                                                reinterpret_cast<double*>(P->nbe_blk.p), slots);
+    CK_LAUNCH();
+    P->nbe_slots = slots;
+    P->has_nbe = true;
+    note_launch(ctx, 2);
+  }
   CK(cudaStreamSynchronize(s));
   note_launch(ctx, 1);
   return P.release();
@@ -2799,7 +2837,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
   for (int r = 0; r < R; ++r)
     if (parts[r]->ctx != ctx) fail(ECT_ERR_SOLVER, "dist_solve: in-process parts must share a context");
   if (comm && R != 1) fail(ECT_ERR_SOLVER, "dist_solve: with a communicator each process owns one part");
-  const int grid_s = grid_for(ctx, nb_fn<K>(ctx->nb_variant, kCocg), kBlock);
+  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], ctx->nb_variant, kCocg), kBlock);
   const int grid_v = DK::vec_grid(ctx);
   const int grid_max = std::max(grid_s, grid_v);
   const int64_t na_g = parts[0]->na_global;
@@ -2890,7 +2928,8 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
       const double2* bp = with_b ? S[r].b.p : nullptr;
       KrylovCtl c = S[r].ctl;
       void* args[] = {&v, &xp, &yp, &bp, &c};
-      CK(cudaLaunchKernel(nb_fn<K>(ctx->nb_variant, mode), dim3(grid_s), dim3(kBlock), args, 0, s));
+      CK(cudaLaunchKernel(part_fn<K>(parts[r], ctx->nb_variant, mode), dim3(grid_s), dim3(kBlock),
+                          args, 0, s));
     }
   };
   auto fin = [&](int what, unsigned mask, int fresh) {
