@@ -168,6 +168,24 @@ int ect_mesh_counts(ect_mesh* mesh, int64_t counts[6]);
  * (the std::set order of apply_essential_bc), canonical connectivity. */
 int ect_mesh_export(ect_mesh* mesh, int32_t* cond_forward, int32_t* pinned_dofs, int32_t* tets);
 
+/* ---- Gmsh ASCII v2.2 files (host only, no GPU needed) ----------------------
+ * load_mesh / write_mesh (mesh_io.hpp:30-38, mesh_io.cpp:68-213) with the
+ * canonical tag map (regions 1..6, boundary labels 11..15): the reader
+ * canonicalises tet orientation and validates like the reference (conformity,
+ * boundary labels equal to classify_boundary) -> ECT_ERR_MESH / ECT_ERR_IO with
+ * "path:line: ..." messages. Feed the arrays to ect_mesh_create. */
+typedef struct ect_gmsh ect_gmsh;
+int ect_gmsh_read(const char* path, ect_gmsh** out);
+/* counts: n_nodes, n_tets, n_boundary_faces */
+int ect_gmsh_counts(ect_gmsh* g, int64_t counts[3]);
+/* any pointer may be NULL; faces/labels in file order (BoundaryLabel values) */
+int ect_gmsh_arrays(ect_gmsh* g, double* xyz, int32_t* tets, uint8_t* region, int32_t* faces,
+                    int32_t* labels);
+int ect_gmsh_destroy(ect_gmsh* g);
+int ect_gmsh_write(const char* path, const double* xyz, int64_t n_nodes, const int32_t* tets,
+                   const uint8_t* region, int64_t n_tets, const int32_t* faces,
+                   const int32_t* labels, int64_t n_faces);
+
 /* ---- materials (host) ---------------------------------------------------
  * RunConfig::material_table + resolve_mu_tilde (config.cpp:325-352),
  * reference_variant (materials.cpp:44-53), and ScanSession's two-config rule

@@ -175,6 +175,46 @@ def make_trace():
     print("trace written", GOLDEN / "trace_small_6x6x12.csv")
 
 
+# The reference's own tube geometry (tube_mesh.cpp:85-270): a steam-generator
+# tube wall with a deposit ring, the probe's coil pair inside the tube — the
+# non-box mesh that SURVEY §8(f)3 asks the GPU path to run.
+TUBE_SPEC = dict(domain_radius=0.03, z_min=-0.02, z_max=0.02, tube_r_inner=0.0085,
+                 tube_r_outer=0.0097, defect=(0.0085, 0.0097, -0.001, 0.001),
+                 coil=(0.006, 0.0075, 0.001, 0.0005), coil_ref_z=0.0,
+                 scan_z=[-0.002, 0.0, 0.002], resolution=6)
+
+
+class _TubeCase:
+    """Duck-typed workload for reference_case: mesh from generate_tube_mesh."""
+    name = "tube_r6"
+    coil = TUBE_SPEC["coil"]
+    positions = (0.0,)
+    amplitude = 1e6
+
+    def __init__(self):
+        self.physics = workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0)
+
+    def mesh(self):
+        rm = ref.RefMesh.tube(TUBE_SPEC)
+        xyz, region = rm.geometry()
+        tets = rm.export()["tets"]
+        return type("TubeMesh", (), {"xyz": xyz, "tets": tets, "region": region})()
+
+
+def make_tube():
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    out = reference_case(_TubeCase(), direct=True)
+    out["tube_spec"] = np.array(json.dumps({k: v for k, v in TUBE_SPEC.items()}))
+    out.update(tube_faces(out))
+    np.savez_compressed(GOLDEN / "tube_r6.npz", **out)
+
+
+def tube_faces(g):
+    """The labelled boundary faces the reference writes to a .msh (write_mesh)."""
+    ex = ref.RefMesh(g["xyz"], g["tets"], g["region"]).export()
+    return {"faces": ex["faces"], "face_labels": ex["face_labels"]}
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "small"
     if what in ("small", "all"):
@@ -185,3 +225,5 @@ if __name__ == "__main__":
         make_cfg1()
     if what in ("trace", "all"):
         make_trace()
+    if what in ("tube", "all"):
+        make_tube()

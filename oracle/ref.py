@@ -104,6 +104,49 @@ class RefMesh:
         _check(lib().ref_mesh_counts(h, C.byref(nn), C.byref(nt), C.byref(nc), C.byref(nf)))
         self.n_nodes, self.n_tets, self.n_cond, self.n_faces = nn.value, nt.value, nc.value, nf.value
 
+    @classmethod
+    def _from_handle(cls, h):
+        self = cls.__new__(cls)
+        self.h = h
+        nn, nt, nc, nf = I64(), I64(), I64(), I64()
+        _check(lib().ref_mesh_counts(h, C.byref(nn), C.byref(nt), C.byref(nc), C.byref(nf)))
+        self.n_nodes, self.n_tets, self.n_cond, self.n_faces = nn.value, nt.value, nc.value, nf.value
+        return self
+
+    @classmethod
+    def tube(cls, spec: dict):
+        """generate_tube_mesh (tube_mesh.cpp:85-270) for a TubeMeshSpec given as a
+        dict with the tube_mesh.hpp:35-57 field names (AnnularBox / CoilPair as
+        4-tuples; absent optionals unset)."""
+        nan = float("nan")
+        box = lambda k: list(spec[k]) if spec.get(k) is not None else [nan] * 4
+        p = np.array([spec["domain_radius"], spec["z_min"], spec["z_max"], spec["tube_r_inner"],
+                      spec["tube_r_outer"], spec.get("tube_z_min", nan), spec.get("tube_z_max", nan),
+                      *box("tsp"), *box("defect"), *spec["coil"], spec.get("coil_ref_z", 0.0),
+                      spec.get("resolution", 8), spec.get("outer_radial_grading", 2.0)], np.float64)
+        scan = np.ascontiguousarray(spec.get("scan_z", ()), np.float64)
+        h = C.c_void_p()
+        _check(lib().ref_tube_mesh_create(_p(p, D), _p(scan, D) if scan.size else None,
+                                          I32(scan.size), C.byref(h)))
+        return cls._from_handle(h)
+
+    @classmethod
+    def load(cls, path):
+        """load_mesh (mesh_io.cpp): Gmsh ASCII 2.2, canonical tag map."""
+        h = C.c_void_p()
+        _check(lib().ref_mesh_load(str(path).encode(), C.byref(h)))
+        return cls._from_handle(h)
+
+    def write(self, path):
+        """write_mesh (mesh_io.cpp)."""
+        _check(lib().ref_mesh_write(self.h, str(path).encode()))
+
+    def geometry(self):
+        xyz = np.empty((self.n_nodes, 3), np.float64)
+        region = np.empty(self.n_tets, np.uint8)
+        _check(lib().ref_mesh_geometry(self.h, _p(xyz, D), _p(region, C.c_uint8)))
+        return xyz, region
+
     def __del__(self):
         if getattr(self, "h", None):
             lib().ref_mesh_destroy(self.h)

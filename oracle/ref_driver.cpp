@@ -32,6 +32,7 @@
 #include "ectsim/element_forms.hpp"
 #include "ectsim/materials.hpp"
 #include "ectsim/mesh.hpp"
+#include "ectsim/mesh_io.hpp"
 #include "ectsim/partition.hpp"
 #include "ectsim/scan.hpp"
 #include "ectsim/signals.hpp"
@@ -181,6 +182,58 @@ int ref_mesh_create(int64_t n_nodes, const double* xyz, int64_t n_tets, const in
 }
 
 void ref_mesh_destroy(void* h) { delete static_cast<RefMesh*>(h); }
+
+// generate_tube_mesh (tube_mesh.cpp:85-270) from a packed TubeMeshSpec:
+// [domain_radius, z_min, z_max, tube_r_inner, tube_r_outer, tube_z_min,
+//  tube_z_max, tsp(r_in, r_out, z_min, z_max), defect(4), coil(r_in, r_out,
+//  height, gap), coil_ref_z, resolution, outer_radial_grading]; NaN = unset.
+int ref_tube_mesh_create(const double* p, const double* scan_z, int32_t n_scan, void** out) {
+  return guarded([&] {
+    TubeMeshSpec spec;
+    spec.domain_radius = p[0];
+    spec.z_min = p[1];
+    spec.z_max = p[2];
+    spec.tube_r_inner = p[3];
+    spec.tube_r_outer = p[4];
+    if (p[5] == p[5]) spec.tube_z_min = p[5];
+    if (p[6] == p[6]) spec.tube_z_max = p[6];
+    if (p[7] == p[7]) spec.tsp = AnnularBox{p[7], p[8], p[9], p[10]};
+    if (p[11] == p[11]) spec.defect = AnnularBox{p[11], p[12], p[13], p[14]};
+    spec.coil = CoilPair{p[15], p[16], p[17], p[18]};
+    spec.coil_ref_z = p[19];
+    spec.resolution = static_cast<int>(p[20]);
+    spec.outer_radial_grading = p[21];
+    spec.scan_z.assign(scan_z, scan_z + n_scan);
+    auto m = std::make_unique<RefMesh>();
+    m->mesh = generate_tube_mesh(spec);
+    m->cmap = conductor_map(m->mesh);
+    *out = m.release();
+  });
+}
+
+// load_mesh / write_mesh (mesh_io.cpp), canonical tag map
+int ref_mesh_load(const char* path, void** out) {
+  return guarded([&] {
+    auto m = std::make_unique<RefMesh>();
+    m->mesh = load_mesh(path);
+    m->cmap = conductor_map(m->mesh);
+    *out = m.release();
+  });
+}
+int ref_mesh_write(void* h, const char* path) {
+  return guarded([&] { write_mesh(static_cast<RefMesh*>(h)->mesh, path); });
+}
+
+// node coordinates and tet regions of a mesh (after canonicalization)
+int ref_mesh_geometry(void* h, double* xyz, uint8_t* region) {
+  return guarded([&] {
+    auto* m = static_cast<RefMesh*>(h);
+    for (int n = 0; n < m->mesh.node_count(); ++n)
+      for (int a = 0; a < 3; ++a) xyz[3 * n + a] = m->mesh.nodes[n][a];
+    for (int t = 0; t < m->mesh.tet_count(); ++t)
+      region[t] = static_cast<uint8_t>(m->mesh.tets[t].region);
+  });
+}
 
 int ref_mesh_counts(void* h, int64_t* n_nodes, int64_t* n_tets, int64_t* n_cond,
                     int64_t* n_boundary_faces) {

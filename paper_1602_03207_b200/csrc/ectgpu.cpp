@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "ect_internal.h"
+#include "mesh_io.h"
 
 namespace {
 
@@ -617,6 +618,70 @@ int ect_delta_impedance(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* prima
       dz[2 * q] = out[q].x;
       dz[2 * q + 1] = out[q].y;
     }
+  });
+}
+
+}  // extern "C"
+
+// ---- Gmsh files ------------------------------------------------------------------
+struct ect_gmsh {
+  ect::GmshMesh m;
+};
+
+extern "C" {
+
+int ect_gmsh_read(const char* path, ect_gmsh** out) {
+  return guarded([&] {
+    require(path != nullptr, ECT_ERR_IO, "ect_gmsh_read: null path");
+    auto g = std::make_unique<ect_gmsh>();
+    g->m = ect::read_gmsh(path);
+    *out = g.release();
+  });
+}
+
+int ect_gmsh_counts(ect_gmsh* g, int64_t counts[3]) {
+  return guarded([&] {
+    counts[0] = (int64_t)g->m.xyz.size() / 3;
+    counts[1] = (int64_t)g->m.region.size();
+    counts[2] = (int64_t)g->m.labels.size();
+  });
+}
+
+int ect_gmsh_arrays(ect_gmsh* g, double* xyz, int32_t* tets, uint8_t* region, int32_t* faces,
+                    int32_t* labels) {
+  return guarded([&] {
+    const auto& m = g->m;
+    if (xyz) std::copy(m.xyz.begin(), m.xyz.end(), xyz);
+    if (tets) std::copy(m.tets.begin(), m.tets.end(), tets);
+    if (region) std::copy(m.region.begin(), m.region.end(), region);
+    if (faces) std::copy(m.faces.begin(), m.faces.end(), faces);
+    if (labels) std::copy(m.labels.begin(), m.labels.end(), labels);
+  });
+}
+
+int ect_gmsh_destroy(ect_gmsh* g) {
+  return guarded([&] { delete g; });
+}
+
+int ect_gmsh_write(const char* path, const double* xyz, int64_t n_nodes, const int32_t* tets,
+                   const uint8_t* region, int64_t n_tets, const int32_t* faces,
+                   const int32_t* labels, int64_t n_faces) {
+  return guarded([&] {
+    require(path != nullptr, ECT_ERR_IO, "ect_gmsh_write: null path");
+    ect::GmshMesh m;
+    m.xyz.assign(xyz, xyz + 3 * n_nodes);
+    m.tets.assign(tets, tets + 4 * n_tets);
+    m.region.assign(region, region + n_tets);
+    for (int64_t t = 0; t < n_tets; ++t)
+      require(m.region[t] < ECT_REGION_COUNT, ECT_ERR_MESH, "ect_gmsh_write: unknown region tag");
+    if (n_faces) {
+      m.faces.assign(faces, faces + 3 * n_faces);
+      m.labels.assign(labels, labels + n_faces);
+      for (int64_t f = 0; f < n_faces; ++f)
+        require(m.labels[f] >= 0 && m.labels[f] < 5, ECT_ERR_MESH,
+                "ect_gmsh_write: unknown boundary label");
+    }
+    ect::write_gmsh(path, m);
   });
 }
 

@@ -181,6 +181,13 @@ class Mesh:
         (self.n_nodes, self.n_tets, self.n_cond, self.n_dofs, self.n_pins,
          self.n_defect) = list(c)
 
+    @classmethod
+    def from_gmsh(cls, ctx: Context, path):
+        """load_mesh (mesh_io.cpp) + the GPU mesh: the file's validated boundary
+        labels equal the geometric classification the device recomputes."""
+        g = read_gmsh(path)
+        return cls(ctx, g["xyz"], g["tets"], g["region"])
+
     def __del__(self):
         if getattr(self, "h", None):
             lib().ect_mesh_destroy(self.h)
@@ -338,6 +345,38 @@ class Session:
                         "z_f3": complex(p.z_f3[0], p.z_f3[1]), "failed": bool(p.failed),
                         "iterations": list(p.iterations)})
         return out
+
+
+# ---- Gmsh ASCII v2.2 files (load_mesh / write_mesh, mesh_io.hpp:30-38) -------------
+def read_gmsh(path) -> dict:
+    """Host-only reader: nodes, canonical tets, regions, labelled boundary faces
+    (validated like the reference's load_mesh)."""
+    h = VP()
+    _check(lib().ect_gmsh_read(str(path).encode(), C.byref(h)))
+    try:
+        c = (I64 * 3)()
+        _check(lib().ect_gmsh_counts(h, c))
+        nn, nt, nf = list(c)
+        out = {"xyz": np.empty((nn, 3), np.float64), "tets": np.empty((nt, 4), np.int32),
+               "region": np.empty(nt, np.uint8), "faces": np.empty((nf, 3), np.int32),
+               "labels": np.empty(nf, np.int32)}
+        _check(lib().ect_gmsh_arrays(h, *[_ptr(out[k]) for k in
+                                          ("xyz", "tets", "region", "faces", "labels")]))
+        return out
+    finally:
+        lib().ect_gmsh_destroy(h)
+
+
+def write_gmsh(path, xyz, tets, region, faces=None, labels=None):
+    """write_mesh's format (%.17g coordinates, canonical tags)."""
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    tets = np.ascontiguousarray(tets, np.int32)
+    region = np.ascontiguousarray(region, np.uint8)
+    faces = np.ascontiguousarray(np.zeros((0, 3)) if faces is None else faces, np.int32)
+    labels = np.ascontiguousarray(np.zeros(0) if labels is None else labels, np.int32)
+    _check(lib().ect_gmsh_write(str(path).encode(), _ptr(xyz), I64(xyz.shape[0]), _ptr(tets),
+                                _ptr(region), I64(tets.shape[0]), _ptr(faces), _ptr(labels),
+                                I64(labels.shape[0])))
 
 
 # ---- distributed solve (row partition over GPUs; SURVEY §8(e)) -------------------

@@ -11,6 +11,9 @@ sys.path.insert(0, str(ROOT))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs under gpurun / round-end GPU tier)")
     config.addinivalue_line("markers", "slow: long-running (full-size configs)")
+    # temporary files (tmp_path) stay inside the repository
+    if not config.option.basetemp:
+        config.option.basetemp = str(Path(__file__).resolve().parent.parent / ".pytest_tmp")
 
 
 @pytest.fixture(scope="session")

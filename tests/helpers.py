@@ -8,7 +8,7 @@ import scipy.sparse as sp
 from scipy.sparse.csgraph import connected_components
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-SMALL = ["small_4x4x8", "small_6x6x12", "small_5x5x10_nodefect"]
+SMALL = ["small_4x4x8", "small_6x6x12", "small_5x5x10_nodefect", "tube_r6"]
 TUBE, TSP, DEFECT = 0, 1, 2
 
 
@@ -61,6 +61,54 @@ def solution_errors(x, x_ref, n_nodes, comp):
     va, vb = mean_free(x[na:]), mean_free(x_ref[na:])
     ev = np.linalg.norm(va - vb) / np.linalg.norm(vb)
     return float(ea), float(ev)
+
+
+def v_errors_sigma(x, x_ref, g, key):
+    """V-part errors that are blind to the near-null modes of weakly conducting
+    regions (the reference configuration gives DEFECT tets sigma_eps =
+    1e-6 sigma_tube, materials.cpp:44-53, so V inside such a region is fixed only
+    ~1e-6 as strongly as in the tube; SURVEY D9's per-component mean-free V then
+    differs between two correct solvers while every physical output agrees):
+      * energy: sqrt(sum_t sigma_t vol_t |grad(V - V*)|^2) / same for V*, over
+        conductor tets (the norm the conduction term induces);
+      * strong: D9's mean-free relative L2 restricted to nodes of well-conducting
+        tets (sigma_t >= 1e-3 max sigma), components over those tets only."""
+    xyz, tets, region, fwd = g["xyz"], g["tets"], g["region"], g["cond_forward"]
+    sigma = np.asarray(g[f"mats_{key}"])[1:7]
+    na = 3 * len(xyz)
+    cond = (region == TUBE) | (region == TSP) | (region == DEFECT)
+    t = tets[cond]
+    st = sigma[region[cond]]
+    P = xyz[t]                                            # [T, 4, 3]
+    J = np.stack([P[:, 1] - P[:, 0], P[:, 2] - P[:, 0], P[:, 3] - P[:, 0]], axis=2)
+    vol = np.abs(np.linalg.det(J)) / 6.0
+    Ginv = np.linalg.inv(J)                               # rows: grad lambda_1..3
+    grads = np.concatenate([-Ginv.sum(axis=1, keepdims=True), Ginv], axis=1)  # [T, 4, 3]
+
+    def grad_v(v):
+        vv = v[na:][fwd[t]]                               # [T, 4]
+        return np.einsum("ta,tad->td", vv, grads)
+
+    gd, gr = grad_v(x) - grad_v(x_ref), grad_v(x_ref)
+    w = st * vol
+    energy = np.sqrt(np.sum(w * np.sum(np.abs(gd) ** 2, axis=1)) /
+                     np.sum(w * np.sum(np.abs(gr) ** 2, axis=1)))
+    strong = st >= 1e-3 * st.max()
+    ts = t[strong]
+    nodes = np.unique(ts.ravel())
+    nc = int(fwd.max()) + 1
+    pairs = [(fwd[ts[:, a]], fwd[ts[:, b]]) for a in range(4) for b in range(4) if a != b]
+    r = np.concatenate([q[0] for q in pairs])
+    c = np.concatenate([q[1] for q in pairs])
+    comp = connected_components(sp.coo_matrix((np.ones_like(r), (r, c)), shape=(nc, nc)),
+                                directed=False)[1]
+    idx = fwd[nodes]
+    va, vb = x[na:][idx].copy(), x_ref[na:][idx].copy()
+    for cc in np.unique(comp[idx]):
+        m = comp[idx] == cc
+        va[m] -= va[m].mean()
+        vb[m] -= vb[m].mean()
+    return float(energy), float(np.linalg.norm(va - vb) / np.linalg.norm(vb))
 
 
 def csr(row_ptr, col, vals):

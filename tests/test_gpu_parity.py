@@ -17,6 +17,7 @@ import pytest
 
 from paper_1602_03207_b200 import ect, workloads
 from tests.helpers import (SMALL, conductor_components, golden, ref_csr_values, ref_matrix,
+                           v_errors_sigma,
                            solution_errors, value_metrics)
 
 pytestmark = pytest.mark.gpu
@@ -156,7 +157,15 @@ def test_solve_matches_direct_reference(ctx, name):
             assert res[c]["converged"], res[c]
             assert res[c]["residual"] <= SOLVE_TOL
             ea, ev = solution_errors(x[:, c], g[f"{key}_x"][c], m.n_nodes, comp)
-            assert ea <= 1e-6 and ev <= 1e-6, (key, c, ea, ev)
+            en, es = v_errors_sigma(x[:, c], g[f"{key}_x"][c], g, key)
+            assert ea <= 1e-6 and en <= 1e-6 and es <= 1e-6, (key, c, ea, en, es)
+            # D9's whole-component mean-free V only where no conductor region is
+            # weak (the reference configuration's sigma_eps DEFECT region on the
+            # tube carries a near-null V mode: 2.4e-4 between two exact solvers)
+            sig = np.asarray(g[f"mats_{key}"])[1:4]
+            present = [r_ for r_ in (0, 1, 2) if (g["region"] == r_).any()]
+            if min(sig[present]) >= 1e-3 * max(sig[present]):
+                assert ev <= 1e-6, (key, c, ev)
             # true residual recomputed on the host with the reference matrix
             rr = np.linalg.norm(g["rhs"][c] - A @ x[:, c]) / np.linalg.norm(g["rhs"][c])
             assert rr <= 2 * SOLVE_TOL, rr
@@ -210,6 +219,23 @@ def test_session_batching_invariance(ctx):
         assert np.max(np.abs(a["dz"] - b["dz"])) <= 1e-7 * np.max(np.abs(a["dz"]))
     again = s.solve_positions(zs, positions_per_batch=1)
     assert all(np.array_equal(a["dz"], b["dz"]) for a, b in zip(one, again))  # repeatable
+
+
+def test_gmsh_tube_through_gpu_path(ctx, tmp_path):
+    """The reference's tube geometry as a Gmsh 2.2 file (write_mesh format)
+    through ect_gmsh_read -> mesh -> assembly: bit-exact reference CSC."""
+    g = golden("tube_r6")
+    path = tmp_path / "tube.msh"
+    ect.write_gmsh(path, g["xyz"], g["tets"], g["region"], g["faces"], g["face_labels"])
+    m = ect.Mesh.from_gmsh(ctx, path)
+    ex = m.export()
+    assert np.array_equal(ex["pinned_dofs"], g["pins"])
+    p, r, _ = m.materials(_physics(g))
+    for key, mats in _configs(g, p, r):
+        cp, ri, v = ect.Matrix(ctx, m).assemble(mats).export_csc()
+        assert cp.tobytes() == g[f"{key}_col_ptr"].tobytes()
+        assert ri.tobytes() == g[f"{key}_row_idx"].tobytes()
+        assert v.tobytes() == g[f"{key}_values"].tobytes()
 
 
 def test_solver_contracts(ctx):
