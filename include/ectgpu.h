@@ -58,8 +58,9 @@ typedef struct ect_materials {
   double delta_gauge;
   double bc_penalty;
   double sigma_eps;
-  int32_t ibc_enabled;       /* must be 0: IBC surface terms are out of scope */
+  int32_t ibc_enabled;       /* impedance condition on the GAMMA_P (plate) faces */
   int32_t l22_use_sigma_eps;
+  double z_surface[2];       /* surface impedance (re, im) used when ibc_enabled */
 } ect_materials;
 
 /* RunConfig [materials] keys (config.hpp:25-39). Negative sigma_defect /
@@ -77,6 +78,7 @@ typedef struct ect_physics {
   double mu_tilde_fixed;
   double sigma_tsp;  /* < 0: default 5e6 (config.hpp:29) */
   double mu_r_tsp;   /* < 0: default 50 (config.hpp:30) */
+  int32_t ibc_tsp;   /* materials.ibc_tsp (config.hpp:38): plate as surface impedance */
 } ect_physics;
 
 /* CoilPair (tube_mesh.hpp:13-21). */

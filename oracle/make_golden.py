@@ -44,7 +44,8 @@ def sha(a: np.ndarray) -> str:
 
 def mats_to_array(m: ref.Materials) -> np.ndarray:
     return np.array([m.omega, *m.sigma, *m.mu, m.mu_tilde, m.delta_gauge, m.bc_penalty,
-                     m.sigma_eps, m.ibc_enabled, m.l22_use_sigma_eps], dtype=np.float64)
+                     m.sigma_eps, m.ibc_enabled, m.l22_use_sigma_eps, *m.z_surface],
+                    dtype=np.float64)
 
 
 def reference_case(w, direct=True, tol=1e-12):
@@ -209,6 +210,33 @@ def make_tube():
     np.savez_compressed(GOLDEN / "tube_r6.npz", **out)
 
 
+# The same tube with a support plate (TSP ring outside the tube) represented
+# by the impedance boundary condition (materials.ibc_tsp, config.cpp:339-345):
+# the non-symmetric A of SURVEY §8(f)4.
+TUBE_IBC_SPEC = dict(TUBE_SPEC, tsp=(0.0105, 0.0200, 0.004, 0.008), resolution=4)
+
+
+class _TubeIbcCase(_TubeCase):
+    name = "tube_ibc_r4"
+
+    def __init__(self):
+        self.physics = workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0, ibc_tsp=True)
+
+    def mesh(self):
+        rm = ref.RefMesh.tube(TUBE_IBC_SPEC)
+        xyz, region = rm.geometry()
+        tets = rm.export()["tets"]
+        return type("TubeMesh", (), {"xyz": xyz, "tets": tets, "region": region})()
+
+
+def make_tube_ibc():
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    out = reference_case(_TubeIbcCase(), direct=True)
+    out["tube_spec"] = np.array(json.dumps({k: v for k, v in TUBE_IBC_SPEC.items()}))
+    out.update(tube_faces(out))
+    np.savez_compressed(GOLDEN / "tube_ibc_r4.npz", **out)
+
+
 def tube_faces(g):
     """The labelled boundary faces the reference writes to a .msh (write_mesh)."""
     ex = ref.RefMesh(g["xyz"], g["tets"], g["region"]).export()
@@ -227,3 +255,5 @@ if __name__ == "__main__":
         make_trace()
     if what in ("tube", "all"):
         make_tube()
+    if what in ("tube_ibc", "all"):
+        make_tube_ibc()

@@ -30,7 +30,8 @@ class Materials(C.Structure):
     _fields_ = [("omega", C.c_double), ("sigma", C.c_double * 6), ("mu", C.c_double * 6),
                 ("mu_tilde", C.c_double), ("delta_gauge", C.c_double),
                 ("bc_penalty", C.c_double), ("sigma_eps", C.c_double),
-                ("ibc_enabled", C.c_int32), ("l22_use_sigma_eps", C.c_int32)]
+                ("ibc_enabled", C.c_int32), ("l22_use_sigma_eps", C.c_int32),
+                ("z_surface", C.c_double * 2)]
 
 
 class Physics(C.Structure):
@@ -39,7 +40,7 @@ class Physics(C.Structure):
                 ("sigma_eps_ratio", C.c_double), ("delta_gauge", C.c_double),
                 ("bc_penalty", C.c_double), ("mu_tilde_harmonic", C.c_int32),
                 ("mu_tilde_fixed", C.c_double), ("sigma_tsp", C.c_double),
-                ("mu_r_tsp", C.c_double)]
+                ("mu_r_tsp", C.c_double), ("ibc_tsp", C.c_int32)]
 
 
 def build_if_possible() -> bool:
@@ -88,7 +89,8 @@ I64 = C.c_int64
 def physics_struct(ph) -> Physics:
     return Physics(ph.frequency, ph.sigma_tube, ph.mu_r_tube, ph.sigma_defect, ph.mu_r_defect,
                    ph.sigma_eps_ratio, ph.delta_gauge, ph.bc_penalty, int(ph.mu_tilde_harmonic),
-                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp)
+                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp,
+                   int(getattr(ph, "ibc_tsp", False)))
 
 
 class RefMesh:

@@ -99,6 +99,7 @@ struct ref_materials {
   double sigma_eps;
   int32_t ibc_enabled;
   int32_t l22_use_sigma_eps;
+  double z_surface[2];  // surface impedance of the plate (IBC), re / im
 };
 
 // The subset of RunConfig [materials] keys (config.hpp:25-39).
@@ -115,6 +116,7 @@ struct ref_physics {
   double mu_tilde_fixed;
   double sigma_tsp;  // < 0: default (config.hpp:29)
   double mu_r_tsp;   // < 0: default (config.hpp:30)
+  int32_t ibc_tsp;   // materials.ibc_tsp (config.hpp:38)
 };
 
 static MaterialTable unpack(const ref_materials* m) {
@@ -130,6 +132,7 @@ static MaterialTable unpack(const ref_materials* m) {
   t.sigma_eps = m->sigma_eps;
   t.ibc_enabled = m->ibc_enabled != 0;
   t.l22_use_sigma_eps = m->l22_use_sigma_eps != 0;
+  t.z_surface = complexd(m->z_surface[0], m->z_surface[1]);
   return t;
 }
 
@@ -146,6 +149,8 @@ static void pack(const MaterialTable& t, ref_materials* m) {
   m->sigma_eps = t.sigma_eps;
   m->ibc_enabled = t.ibc_enabled;
   m->l22_use_sigma_eps = t.l22_use_sigma_eps;
+  m->z_surface[0] = t.z_surface.real();
+  m->z_surface[1] = t.z_surface.imag();
 }
 
 extern "C" {
@@ -284,6 +289,7 @@ int ref_materials_from_physics(void* h, const ref_physics* p, ref_materials* pri
     cfg.mu_tilde_fixed = p->mu_tilde_fixed;
     if (p->sigma_tsp >= 0) cfg.sigma_tsp = p->sigma_tsp;
     if (p->mu_r_tsp >= 0) cfg.mu_r_tsp = p->mu_r_tsp;
+    cfg.ibc_tsp = p->ibc_tsp != 0;
     MaterialTable mats = cfg.material_table();
     cfg.resolve_mu_tilde(mats, m->mesh);
     MaterialTable ref = reference_variant(mats);

@@ -65,9 +65,10 @@ struct DevBuf {
 
 // Device-side per-right-hand-side Krylov state (see krylov.cu).
 struct RhsState {
-  double2 rho;    // r^T z (unconjugated, COCG)
+  double2 rho;    // r^T z (unconjugated, COCG); (r_hat, r) in BiCGStab
   double2 alpha;
   double2 beta;
+  double2 omega;  // BiCGStab stabilisation step
   double bnorm;
   double rnorm;
   int iters;
@@ -106,6 +107,7 @@ struct ect_ctx {
   int sell_sigma = 256;
   struct SolverWorkspace {                      // cocg_solve buffers, reused across solves
     ect::DevBuf<double2> bb, xx, r, p, q;
+    ect::DevBuf<double2> rh, ph, sh, t;         // BiCGStab extras
     ect::DevBuf<ect::RhsState> st;
     ect::DevBuf<int> n_active;
     ect::DevBuf<unsigned> counter;
@@ -137,6 +139,15 @@ struct ect_mesh {
   std::vector<uint8_t> h_region;
   double z_lo = 0.0, z_hi = 0.0;
   int max_inc = 0, max_nbr = 0;
+  // impedance (GAMMA_P) faces, built on first IBC assembly (assembly.cu):
+  // sorted node triples in classify_boundary's order, their TriFrames, and
+  // per node the incident faces ascending (entry = 4 * face + position)
+  bool have_ibc = false;
+  int64_t n_ibc = 0;
+  ect::DevBuf<int> ibc_nodes;      // [n_ibc][3]
+  ect::DevBuf<double> ibc_frame;   // [n_ibc][13]: area, normal[3], grad_tau[3][3]
+  ect::DevBuf<int> ibc_off;        // n_nodes + 1
+  ect::DevBuf<int> ibc_inc;
 };
 
 struct ect_matrix {
@@ -145,6 +156,7 @@ struct ect_matrix {
   int64_t n_nodes = 0, n_cond = 0;  // DOF structure when built from a mesh
   bool from_mesh = false;
   bool assembled = false;
+  bool symmetric = true;  // false with impedance surface terms (va = i omega av^T)
   ect::DevBuf<int> row_ptr;
   ect::DevBuf<int> col;
   ect::DevBuf<double2> val;

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -126,7 +127,8 @@ bool same_coefficients(const ect_materials& a, const ect_materials& b) {
   // MaterialTable::same_coefficients (materials.cpp:24-30)
   if (a.omega != b.omega || a.mu_tilde != b.mu_tilde || a.delta_gauge != b.delta_gauge ||
       a.bc_penalty != b.bc_penalty || a.sigma_eps != b.sigma_eps ||
-      a.ibc_enabled != b.ibc_enabled || a.l22_use_sigma_eps != b.l22_use_sigma_eps)
+      a.ibc_enabled != b.ibc_enabled || a.l22_use_sigma_eps != b.l22_use_sigma_eps ||
+      a.z_surface[0] != b.z_surface[0] || a.z_surface[1] != b.z_surface[1])
     return false;
   for (int r = 0; r < ECT_REGION_COUNT; ++r)
     if (a.sigma[r] != b.sigma[r] || a.mu[r] != b.mu[r]) return false;
@@ -134,9 +136,9 @@ bool same_coefficients(const ect_materials& a, const ect_materials& b) {
 }
 
 void check_materials(const ect_materials& m) {
-  if (m.ibc_enabled) {
-    ect::fail(ECT_ERR_CONFIG,
-              "ibc_enabled: impedance surface terms are not supported by the GPU path");
+  if (m.ibc_enabled && m.z_surface[0] == 0.0 && m.z_surface[1] == 0.0) {
+    // element_ibc (element_forms.cpp:117-119)
+    ect::fail(ECT_ERR_SOLVER, "impedance surface term with zero surface impedance");
   }
   require(m.omega > 0.0, ECT_ERR_CONFIG, "materials: omega must be positive");
   require(m.mu_tilde > 0.0, ECT_ERR_CONFIG, "materials: mu_tilde must be positive");
@@ -430,6 +432,20 @@ int ect_materials_from_physics(ect_mesh* mesh, const ect_physics* ph, ect_materi
     set(ECT_REGION_COIL1, 0.0, kMu0);
     set(ECT_REGION_COIL2, 0.0, kMu0);
     set(ECT_REGION_VACUUM, 0.0, kMu0);
+    if (ph->ibc_tsp) {
+      // config.cpp:339-345: the plate volume is assembled as vacuum and
+      // represented by the surface impedance of its material (materials.cpp:12-22)
+      const double s_tsp = ph->sigma_tsp >= 0 ? ph->sigma_tsp : 5e6;
+      const double mu_tsp = kMu0 * (ph->mu_r_tsp >= 0 ? ph->mu_r_tsp : 50.0);
+      require(m.omega > 0.0 && mu_tsp > 0.0 && s_tsp > 0.0, ECT_ERR_CONFIG,
+              "skin_depth requires positive omega, mu, sigma");
+      const double delta = std::sqrt(2.0 / (m.omega * mu_tsp * s_tsp));
+      const std::complex<double> z = std::complex<double>(1.0, -1.0) / (delta * s_tsp);
+      m.ibc_enabled = 1;
+      m.z_surface[0] = z.real();
+      m.z_surface[1] = z.imag();
+      set(ECT_REGION_TSP, m.sigma_eps, kMu0);
+    }
     // resolve_mu_tilde (config.cpp:349-352)
     if (ph->mu_tilde_harmonic) {
       int rc = ect_harmonic_mu_tilde(mesh, &m, &m.mu_tilde);

@@ -2089,6 +2089,7 @@ size_t nbs_bytes(const NbsCfg& c, ect_matrix* a, int mode) {
 
 template <int K>
 struct Dispatch {
+  static constexpr int kWidth = K;
   static constexpr bool kNbOk = K <= 8;
   static constexpr bool kNbtOk = K <= 4;
   static bool use_nbt(const ect_matrix* a) {
@@ -2484,10 +2485,368 @@ void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
   prof_collect(ctx);
 }
 
+// ---- BiCGStab (non-symmetric A: impedance surface terms) ----------------------
+// With element_ibc the coupling blocks satisfy va = i*omega*av^T, so A != A^T
+// and COCG does not apply; the reference still runs GMRES(80)+ILU(0)
+// (iterative.cpp:109-228). The GPU runs right-Jacobi-preconditioned BiCGStab
+// (conjugated inner products), k right-hand sides interleaved, device-resident
+// scalars, the same convergence contract (recurrence residual, then a true
+// residual with restart) and the same breakdown-as-error rule.
+namespace {
+
+__device__ __forceinline__ double2 cconj_mul(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+// Elementwise kernels: thread owns element e = i*K + k of [n][K] vectors; the
+// grid stride is a multiple of K, so k = lane % K is fixed per thread.
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_bi_p(int64_t n, const double2* __restrict__ r, double2* __restrict__ p,
+       const double2* __restrict__ v, double2* __restrict__ ph, const double2* __restrict__ dinv,
+       KrylovCtl ctl) {
+  if (*ctl.n_active == 0) return;
+  const int k = (threadIdx.x & 31) % K;
+  const RhsState st = ctl.st[k];
+  if (st.status != kActive) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 pn = cadd(r[e], cmul(st.beta, csub(p[e], cmul(st.omega, v[e]))));
+    p[e] = pn;
+    ph[e] = cmul(dinv[e / K], pn);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_bi_s(int64_t n, double2* __restrict__ r, const double2* __restrict__ v,
+       double2* __restrict__ sh, const double2* __restrict__ dinv, KrylovCtl ctl) {
+  if (*ctl.n_active == 0) return;
+  const int k = (threadIdx.x & 31) % K;
+  const RhsState st = ctl.st[k];
+  if (st.status != kActive) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 s = csub(r[e], cmul(st.alpha, v[e]));
+    r[e] = s;
+    sh[e] = cmul(dinv[e / K], s);
+  }
+}
+
+// WHAT 0: (a, b) -> alpha = rho / (r_hat, v)
+// WHAT 1: (t, s), (t, t) -> omega
+template <int K, int WHAT>
+__global__ void __launch_bounds__(kBlock)
+k_bi_dot(int64_t n, const double2* __restrict__ a, const double2* __restrict__ b, KrylovCtl ctl) {
+  constexpr int NVL = WHAT == 0 ? 2 : 3, NV = NVL * K;
+  __shared__ double smem[32 * NV];
+  if (*ctl.n_active == 0) return;
+  const int k = (threadIdx.x & 31) % K;
+  const bool act = ctl.st[k].status == kActive;
+  double part[NVL];
+#pragma unroll
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
+  if (act)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const double2 av = a[e], bv = b[e];
+      const double2 d = cconj_mul(av, bv);
+      part[0] += d.x;
+      part[1] += d.y;
+      if (WHAT == 1) part[2] += av.x * av.x + av.y * av.y;
+    }
+  double bsum[NV];
+  block_sum_slots<NVL, K>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    int active = 0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      RhsState& s = ctl.st[c];
+      if (s.status != kActive) continue;
+      const double2 d = make_double2(tot[NVL * c], tot[NVL * c + 1]);
+      if (WHAT == 0) {
+        if (d.x == 0.0 && d.y == 0.0) { s.status = kBreakdown; continue; }
+        s.alpha = cdiv(s.rho, d);
+      } else {
+        const double tt = tot[NVL * c + 2];
+        s.omega = tt > 0.0 ? cdiv(d, make_double2(tt, 0.0)) : make_double2(0.0, 0.0);
+      }
+      ++active;
+    }
+    *ctl.n_active = active;
+    *ctl.counter = 0u;
+  }
+}
+
+// x += alpha p_hat + omega s_hat ; r = s - omega t ; rho_new = (r_hat, r), ||r||
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_bi_x(int64_t n, double2* __restrict__ x, double2* __restrict__ r,
+       const double2* __restrict__ ph, const double2* __restrict__ sh,
+       const double2* __restrict__ t, const double2* __restrict__ rh, KrylovCtl ctl) {
+  constexpr int NVL = 3, NV = NVL * K;
+  __shared__ double smem[32 * NV];
+  if (*ctl.n_active == 0) return;
+  const int k = (threadIdx.x & 31) % K;
+  const RhsState st = ctl.st[k];
+  const bool act = st.status == kActive;
+  double part[NVL] = {0.0, 0.0, 0.0};
+  if (act)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      x[e] = cadd(x[e], cadd(cmul(st.alpha, ph[e]), cmul(st.omega, sh[e])));
+      const double2 rn = csub(r[e], cmul(st.omega, t[e]));
+      r[e] = rn;
+      const double2 d = cconj_mul(rh[e], rn);
+      part[0] += d.x;
+      part[1] += d.y;
+      part[2] += rn.x * rn.x + rn.y * rn.y;
+    }
+  double bsum[NV];
+  block_sum_slots<NVL, K>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    int active = 0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      RhsState& s = ctl.st[c];
+      if (s.status != kActive) continue;
+      const double2 rho_new = make_double2(tot[NVL * c], tot[NVL * c + 1]);
+      s.rnorm = sqrt(tot[NVL * c + 2]);
+      s.iters += 1;
+      if (s.rnorm <= ctl.tol * s.bnorm) {
+        s.status = kConverged;
+      } else if (s.iters >= ctl.max_iter) {
+        s.status = kMaxIter;
+      } else if ((rho_new.x == 0.0 && rho_new.y == 0.0) || (s.omega.x == 0.0 && s.omega.y == 0.0)) {
+        s.status = kBreakdown;
+      } else {
+        s.beta = cmul(cdiv(rho_new, s.rho), cdiv(s.alpha, s.omega));
+        s.rho = rho_new;
+        ++active;
+      }
+    }
+    *ctl.n_active = active;
+    *ctl.counter = 0u;
+  }
+}
+
+// (re)start masked columns from r (fresh: x = 0, r = b, bnorm): r_hat = r,
+// p = v = 0, rho = (r_hat, r), alpha = omega = 1, beta = 0
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_bi_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x,
+           double2* __restrict__ r, double2* __restrict__ rh, double2* __restrict__ p,
+           double2* __restrict__ v, unsigned mask, int fresh, KrylovCtl ctl) {
+  constexpr int NVL = 3, NV = NVL * K;
+  __shared__ double smem[32 * NV];
+  const int k = (threadIdx.x & 31) % K;
+  const bool on = (mask >> k) & 1u;
+  double part[NVL] = {0.0, 0.0, 0.0};
+  if (on)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      double2 rv;
+      if (fresh) {
+        rv = b[e];
+        x[e] = make_double2(0.0, 0.0);
+        r[e] = rv;
+      } else {
+        rv = r[e];
+      }
+      rh[e] = rv;
+      p[e] = v[e] = make_double2(0.0, 0.0);
+      part[0] += rv.x * rv.x + rv.y * rv.y;  // (r_hat, r) = ||r||^2
+    }
+  double bsum[NV];
+  block_sum_slots<NVL, K>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    int active = 0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      RhsState& s = ctl.st[c];
+      if ((mask >> c) & 1u) {
+        const double rr = tot[NVL * c];
+        if (fresh) {
+          s.bnorm = sqrt(rr);
+          s.iters = 0;
+        }
+        s.rnorm = sqrt(rr);
+        s.rho = make_double2(rr, 0.0);
+        s.alpha = s.omega = make_double2(1.0, 0.0);
+        s.beta = make_double2(0.0, 0.0);
+        if (fresh && s.bnorm == 0.0) s.status = kZeroRhs;
+        else if (s.rnorm <= ctl.tol * s.bnorm) s.status = kConverged;
+        else s.status = kActive;
+      }
+      active += s.status == kActive;
+    }
+    *ctl.n_active = active;
+    *ctl.counter = 0u;
+  }
+}
+
+template <int K>
+void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
+                const ect_iter_options& opt, SolveOut* out) {
+  using DK = Dispatch<K>;
+  const int64_t n = a->n;
+  cudaStream_t s = ctx->stream;
+  const int grid_s = DK::spmv_grid(ctx, kPlain, a);
+  const int grid_r = DK::spmv_grid(ctx, kResid, a);
+  const int grid_v = grid_for(ctx, (const void*)k_bi_x<K>, kBlock);
+  const int grid_max = std::max(std::max(grid_s, grid_r), grid_v);
+  const size_t vec = (size_t)n * K;
+  auto& W = ctx->ws;
+  for (auto* v : {&W.bb, &W.xx, &W.r, &W.p, &W.q, &W.rh, &W.ph, &W.sh, &W.t}) v->ensure(vec);
+  W.st.ensure(K);
+  W.n_active.ensure(1);
+  W.counter.ensure(1);
+  W.partial.ensure((size_t)grid_max * 4 * K);
+  CK(cudaMemsetAsync(W.st.p, 0, W.st.bytes(), s));
+  CK(cudaMemsetAsync(W.counter.p, 0, sizeof(unsigned), s));
+  if (K == k) {
+    CK(cudaMemcpyAsync(W.bb.p, b, vec * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  } else {
+    CK(cudaMemsetAsync(W.bb.p, 0, W.bb.bytes(), s));
+    CK(cudaMemcpy2DAsync(W.bb.p, K * sizeof(double2), b, k * sizeof(double2), k * sizeof(double2),
+                         n, cudaMemcpyDeviceToDevice, s));
+  }
+  KrylovCtl ctl{W.st.p, W.n_active.p, W.counter.p, W.partial.p, opt.tol, opt.max_iter,
+                nullptr, 0, n, n, n};
+  const unsigned all = (K == 32) ? 0xffffffffu : ((1u << K) - 1u);
+  // v lives in q
+  k_bi_start<K><<<grid_v, kBlock, 0, s>>>(n, W.bb.p, W.xx.p, W.r.p, W.rh.p, W.p.p, W.q.p, all, 1,
+                                          ctl);
+  CK_LAUNCH();
+  note_launch(ctx, 1);
+  std::vector<int> last_break(K, -1);
+  std::vector<RhsState> hs(K);
+  int* flag = ctx->pinned_flag;
+  const int chunk = 16;
+  for (int restart_round = 0;; ++restart_round) {
+    int polls = 0, launched = 0;
+    cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
+    const int cap = opt.max_iter + chunk;
+    for (; opt.max_iter > 0;) {
+      for (int it = 0; it < chunk; ++it) {
+        k_bi_p<K><<<grid_v, kBlock, 0, s>>>(n, W.r.p, W.p.p, W.q.p, W.ph.p, a->dinv.p, ctl);
+        DK::spmv(ctx, kPlain, grid_s, n, a, W.ph.p, W.q.p, nullptr, ctl);
+        k_bi_dot<K, 0><<<grid_v, kBlock, 0, s>>>(n, W.rh.p, W.q.p, ctl);
+        k_bi_s<K><<<grid_v, kBlock, 0, s>>>(n, W.r.p, W.q.p, W.sh.p, a->dinv.p, ctl);
+        DK::spmv(ctx, kPlain, grid_s, n, a, W.sh.p, W.t.p, nullptr, ctl);
+        k_bi_dot<K, 1><<<grid_v, kBlock, 0, s>>>(n, W.t.p, W.r.p, ctl);
+        k_bi_x<K><<<grid_v, kBlock, 0, s>>>(n, W.xx.p, W.r.p, W.ph.p, W.sh.p, W.t.p, W.rh.p, ctl);
+        CK_LAUNCH();
+        note_launch(ctx, 7);
+      }
+      launched += chunk;
+      CK(cudaMemcpyAsync(flag + (polls & 1), W.n_active.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(poll_ev[polls & 1], s));
+      ++polls;
+      if (polls >= 2) {
+        const int prev = (polls - 2) & 1;
+        CK(cudaEventSynchronize(poll_ev[prev]));
+        if (flag[prev] == 0) break;
+      }
+      if (launched > cap + 2 * chunk) break;
+    }
+    CK(cudaStreamSynchronize(s));
+    // true residual confirmation (iterative.cpp:208-216): q <- b - A x
+    CK(cudaMemsetAsync(W.n_active.p, 0xff, sizeof(int), s));
+    CK(cudaMemcpyAsync(hs.data(), W.st.p, K * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    {
+      std::vector<RhsState> tmp = hs;
+      for (auto& t : tmp) t.status = kActive;
+      CK(cudaMemcpyAsync(W.st.p, tmp.data(), K * sizeof(RhsState), cudaMemcpyHostToDevice, s));
+      DK::spmv(ctx, kResid, grid_r, n, a, W.xx.p, W.q.p, W.bb.p, ctl);
+      note_launch(ctx, 1);
+      std::vector<RhsState> res(K);
+      CK(cudaMemcpyAsync(res.data(), W.st.p, K * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int c = 0; c < K; ++c) hs[c].rnorm = res[c].rnorm;
+      CK(cudaMemcpyAsync(W.st.p, hs.data(), K * sizeof(RhsState), cudaMemcpyHostToDevice, s));
+    }
+    unsigned restart_mask = 0;
+    for (int c = 0; c < k; ++c) {
+      RhsState& t = hs[c];
+      const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
+      if (t.status == kBreakdown) {
+        // a (near-)breakdown of the Lanczos recurrences: restart from the true
+        // residual (new shadow vector); an error only when it recurs at once
+        if (restart_round >= 32 || t.iters >= opt.max_iter || t.iters == last_break[c])
+          fail(ECT_ERR_SOLVER, "BiCGStab breakdown on right-hand side " + std::to_string(c));
+        last_break[c] = t.iters;
+        restart_mask |= 1u << c;
+        continue;
+      }
+      if (t.status == kConverged && rel > opt.tol && t.iters < opt.max_iter && restart_round < 32)
+        restart_mask |= 1u << c;
+    }
+    if (!restart_mask) break;
+    for (int c = 0; c < K; ++c)
+      if ((restart_mask >> c) & 1u)
+        CK(cudaMemcpy2DAsync(W.r.p + c, K * sizeof(double2), W.q.p + c, K * sizeof(double2),
+                             sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
+    k_bi_start<K><<<grid_v, kBlock, 0, s>>>(n, W.bb.p, W.xx.p, W.r.p, W.rh.p, W.p.p, W.q.p,
+                                            restart_mask, 0, ctl);
+    CK_LAUNCH();
+    note_launch(ctx, 1);
+    CK(cudaStreamSynchronize(s));
+  }
+  for (int c = 0; c < k; ++c) {
+    const RhsState& t = hs[c];
+    out->iters[c] = t.iters;
+    const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
+    out->residual[c] = rel;
+    out->converged[c] = (t.status == kZeroRhs) || (t.status == kConverged && rel <= opt.tol);
+  }
+  if (K == k) {
+    CK(cudaMemcpyAsync(x, W.xx.p, vec * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  } else {
+    CK(cudaMemcpy2DAsync(x, k * sizeof(double2), W.xx.p, K * sizeof(double2), k * sizeof(double2),
+                         n, cudaMemcpyDeviceToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
 void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
                 const ect_iter_options& opt, SolveOut* out) {
   if (!(opt.tol > 0.0)) fail(ECT_ERR_SOLVER, "solve_iterative: tolerance must be positive");
   if (k < 1 || k > 16) fail(ECT_ERR_SOLVER, "solve: n_rhs must be in 1..16");
+  if (!a->symmetric) {  // impedance surface terms: A != A^T
+    out->iters.assign(k, 0);
+    out->residual.assign(k, 0.0);
+    out->converged.assign(k, 0);
+    int kb = 1;
+    while (kb < k) kb <<= 1;
+    with_k(kb, [&](auto D) {
+      using DK = decltype(D);
+      constexpr int KK = DK::kWidth;
+      bicgstab_k<KK>(ctx, a, b, x, k, opt, out);
+    });
+    return;
+  }
   int kk = 1;
   while (kk < k) kk <<= 1;  // internal batch width (padding columns stay at b = 0)
   const int64_t n = a->n;

@@ -52,14 +52,14 @@ class Materials(C.Structure):
     """ect_materials == MaterialTable (materials.hpp:21-48)."""
     _fields_ = [("omega", D), ("sigma", D * 6), ("mu", D * 6), ("mu_tilde", D),
                 ("delta_gauge", D), ("bc_penalty", D), ("sigma_eps", D),
-                ("ibc_enabled", I32), ("l22_use_sigma_eps", I32)]
+                ("ibc_enabled", I32), ("l22_use_sigma_eps", I32), ("z_surface", D * 2)]
 
 
 class Physics(C.Structure):
     _fields_ = [("frequency", D), ("sigma_tube", D), ("mu_r_tube", D), ("sigma_defect", D),
                 ("mu_r_defect", D), ("sigma_eps_ratio", D), ("delta_gauge", D),
                 ("bc_penalty", D), ("mu_tilde_harmonic", I32), ("mu_tilde_fixed", D),
-                ("sigma_tsp", D), ("mu_r_tsp", D)]
+                ("sigma_tsp", D), ("mu_r_tsp", D), ("ibc_tsp", I32)]
 
 
 class Coil(C.Structure):
@@ -117,7 +117,8 @@ def _ptr(a):
 def physics_struct(ph) -> Physics:
     return Physics(ph.frequency, ph.sigma_tube, ph.mu_r_tube, ph.sigma_defect, ph.mu_r_defect,
                    ph.sigma_eps_ratio, ph.delta_gauge, ph.bc_penalty, int(ph.mu_tilde_harmonic),
-                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp)
+                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp,
+                   int(getattr(ph, "ibc_tsp", False)))
 
 
 class Context:

@@ -42,6 +42,7 @@ class Physics:
     mu_tilde_fixed: float = 1.25663706212e-6
     sigma_tsp: float = -1.0      # <0: default (config.hpp:29)
     mu_r_tsp: float = -1.0
+    ibc_tsp: bool = False        # plate as a surface impedance (config.hpp:38)
 
 
 @dataclass

@@ -9,6 +9,8 @@ from scipy.sparse.csgraph import connected_components
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 SMALL = ["small_4x4x8", "small_6x6x12", "small_5x5x10_nodefect", "tube_r6"]
+# impedance-boundary (non-symmetric) fixtures: reference build only, no numpy port
+IBC = ["tube_ibc_r4"]
 TUBE, TSP, DEFECT = 0, 1, 2
 
 

@@ -33,8 +33,9 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     from paper_1602_03207_b200 import ect
-    # ect_materials: 17 doubles + 2 int32 (materials.hpp:21-48 field order)
-    assert ctypes.sizeof(ect.Materials) == 17 * 8 + 8
+    # ect_materials: 17 doubles + 2 int32 + complex z_surface (materials.hpp:21-48 order)
+    assert ctypes.sizeof(ect.Materials) == 17 * 8 + 8 + 16
+    assert ctypes.sizeof(ect.Physics) == ctypes.sizeof(__import__("oracle.ref").ref.Physics)
     assert ctypes.sizeof(ect.SignalPoint) == 8 * 13 + 4 * 5 + 4  # padded to 8
     from oracle import ref
     assert ctypes.sizeof(ref.Materials) == ctypes.sizeof(ect.Materials)

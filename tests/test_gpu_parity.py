@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 from paper_1602_03207_b200 import ect, workloads
-from tests.helpers import (SMALL, conductor_components, golden, ref_csr_values, ref_matrix,
+from tests.helpers import (IBC, SMALL, conductor_components, golden, ref_csr_values, ref_matrix,
                            v_errors_sigma,
                            solution_errors, value_metrics)
 
@@ -31,7 +31,10 @@ def _mesh(ctx, g):
 
 def _physics(g):
     has_defect = bool((g["region"] == 2).any())
-    return workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0) if has_defect else workloads.Physics()
+    ibc = bool(g["mats_primary"][17])
+    if has_defect:
+        return workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0, ibc_tsp=ibc)
+    return workloads.Physics(ibc_tsp=ibc)
 
 
 def _configs(g, p, r):
@@ -39,7 +42,7 @@ def _configs(g, p, r):
     return list(zip(keys, (p, r)))
 
 
-@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("name", SMALL + IBC)
 def test_mesh_prep_matches_reference(ctx, name):
     g = golden(name)
     m = _mesh(ctx, g)
@@ -50,10 +53,15 @@ def test_mesh_prep_matches_reference(ctx, name):
     p, r, two = m.materials(_physics(g))
     assert two == bool(g["two_configs"])
     assert p.mu_tilde == g["mats_primary"][13]                            # harmonic mu_tilde, exact
+    assert p.ibc_enabled == int(g["mats_primary"][17])
+    if p.ibc_enabled:                                                     # surface_impedance, exact
+        assert (p.z_surface[0], p.z_surface[1]) == tuple(g["mats_primary"][19:21])
+        assert (r.z_surface[0], r.z_surface[1]) == tuple(g["mats_reference"][19:21])
+        assert list(p.sigma) == list(g["mats_primary"][1:7])              # plate assembled as sigma_eps
     assert m.n_defect == int((g["region"] == 2).sum())
 
 
-@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("name", SMALL + IBC)
 def test_pattern_and_values_bit_exact(ctx, name):
     g = golden(name)
     m = _mesh(ctx, g)
@@ -76,7 +84,7 @@ def test_pattern_and_values_bit_exact(ctx, name):
         assert v2.tobytes() == g[f"{key}_values"].tobytes()
 
 
-@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("name", SMALL + IBC)
 def test_rhs_matches_reference(ctx, name):
     g = golden(name)
     m = _mesh(ctx, g)
@@ -90,7 +98,7 @@ def test_rhs_matches_reference(ctx, name):
         assert np.all(b[g["pins"], c] == 0)                            # pinned entries
 
 
-@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("name", SMALL + IBC)
 def test_spmv_matches_reference_multiply(ctx, name):
     g = golden(name)
     A = ref_matrix(g).tocsr()
@@ -142,20 +150,24 @@ def test_storage_formats_spmv_and_solve(fmt):
         assert np.max(np.abs(gm.multiply(x) - A @ x) / (absA @ np.abs(x))) <= 1e-14
 
 
-@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("name", SMALL + IBC)
 def test_solve_matches_direct_reference(ctx, name):
     g = golden(name)
     m = _mesh(ctx, g)
     comp = conductor_components(g["tets"], g["region"], g["cond_forward"])
     p, r, two = m.materials(_physics(g))
+    # With the impedance condition the V block is ill-conditioned (a 1e-10
+    # relative change of b moves V by up to 1e-4 in the conduction-energy norm,
+    # LU vs LU), so that fixture is solved (BiCGStab) to 1e-13 instead.
+    tol = 1e-13 if name in IBC else SOLVE_TOL
     for key, mats in _configs(g, p, r):
         a = ect.Matrix(ctx, m).assemble(mats)
         A = ref_matrix(g, key)
         b = np.ascontiguousarray(g["rhs"].T)
-        x, res = a.solve(b, tol=SOLVE_TOL, max_iter=20000)
+        x, res = a.solve(b, tol=tol, max_iter=40000)
         for c in range(2):
             assert res[c]["converged"], res[c]
-            assert res[c]["residual"] <= SOLVE_TOL
+            assert res[c]["residual"] <= tol
             ea, ev = solution_errors(x[:, c], g[f"{key}_x"][c], m.n_nodes, comp)
             en, es = v_errors_sigma(x[:, c], g[f"{key}_x"][c], g, key)
             assert ea <= 1e-6 and en <= 1e-6 and es <= 1e-6, (key, c, ea, en, es)
@@ -168,10 +180,10 @@ def test_solve_matches_direct_reference(ctx, name):
                 assert ev <= 1e-6, (key, c, ev)
             # true residual recomputed on the host with the reference matrix
             rr = np.linalg.norm(g["rhs"][c] - A @ x[:, c]) / np.linalg.norm(g["rhs"][c])
-            assert rr <= 2 * SOLVE_TOL, rr
+            assert rr <= 2 * tol, rr
 
 
-@pytest.mark.parametrize("name", ["small_4x4x8", "small_6x6x12"])
+@pytest.mark.parametrize("name", ["small_4x4x8", "small_6x6x12", "tube_ibc_r4"])
 def test_delta_impedance_and_session(ctx, name):
     g = golden(name)
     m = _mesh(ctx, g)
@@ -280,5 +292,5 @@ def test_error_paths(ctx):
         ect.Mesh(ctx, g["xyz"], g["tets"], np.full_like(g["region"], 5))
     p, r, _ = m.materials(_physics(g))
     p.ibc_enabled = 1
-    with pytest.raises(ect.ConfigError):  # IBC surface terms are out of scope
+    with pytest.raises(ect.SolverError):  # element_ibc: zero surface impedance
         ect.Matrix(ctx, m).assemble(p)
