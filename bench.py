@@ -329,8 +329,14 @@ def cpu_baseline_leg(a, mesh, w, positions, threads):
         out = rs.solve_iterative_batch(bs, tol=TOL, max_iter=max_iter, restart=80,
                                        threads=nthreads)
         its = int(out["iterations"].sum())
+        # the reference's CscMatrix::multiply, single thread
+        xs = np.ascontiguousarray(b[:, 0])
+        _, t_mv = rs.multiply(xs, repeat=3)
+        b_mv = 20 * a.nnz + 4 * (a.n + 1) + 32 * a.n
         return {"value": a.n * its / out["seconds"], "unit": UNIT, "cores": nthreads,
                 "kind": "reference",
+                "spmv_single_thread_GBps": b_mv / (t_mv / 3) / 1e9,
+                "spmv_single_thread_ms": t_mv / 3 * 1e3,
                 "sample": f"{nthreads} concurrent solve_iterative calls (GMRES(80)+ILU(0), "
                           f"ILU rebuilt per call as iterative.cpp:126) x {max_iter} iterations "
                           f"on the configs[1] primary matrix; {out['seconds']:.1f} s wall"}

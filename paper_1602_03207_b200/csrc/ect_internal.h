@@ -101,6 +101,8 @@ struct ect_ctx {
   int* pinned_flag = nullptr;  // small pinned word for convergence polling
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
+  cudaStream_t halo_stream = nullptr;           // distributed solve: halo exchange
+  cudaEvent_t ev_h1 = nullptr, ev_h2 = nullptr;
   bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
   bool use_sell = false;                        // ect_ctx_set_format(ctx, ECT_FORMAT_SELL)
   bool use_nbe = true;                          // NB-E sliced-ELL blocks (default; variants 1..49 off)
@@ -204,6 +206,7 @@ struct ect_part {
   ect::DevBuf<int> blk_ptr, blk_col, cpl_ptr, cond_local;
   ect::DevBuf<int2> cpl_idx;
   ect::DevBuf<double2> blk, cpl, dinv;  // NB planes (3 x 4 doubles, 2 x 4 doubles), local dinv
+  int64_t int_lo = 0, int_hi = 0;        // interior owned nodes (no ghost columns)
   bool has_nbe = false;                  // sliced-ELL copy of blk (default SpMV layout)
   int64_t nbe_slots = 0;
   ect::DevBuf<int> nbe_off, nbe_col;

@@ -218,6 +218,9 @@ int ect_ctx_destroy(ect_ctx* ctx) {
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     for (auto e : ctx->marks) cudaEventDestroy(e);
+    if (ctx->ev_h1) cudaEventDestroy(ctx->ev_h1);
+    if (ctx->ev_h2) cudaEventDestroy(ctx->ev_h2);
+    if (ctx->halo_stream) cudaStreamDestroy(ctx->halo_stream);
     ctx->cub_tmp.release();
     cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -155,6 +155,8 @@ struct KrylovCtl {
   double* red;
   // owned rows of the vector kernels: [s0, e0) U [s1, e1)
   int64_t s0, e0, s1, e1;
+  // split SpMV (halo overlap): later launches add their totals into red
+  int red_add;
 };
 
 // ---- scalar finalisations (run by one thread on the global totals) ----------
@@ -386,6 +388,7 @@ struct NbView {
   int64_t n_nodes;  // nodes whose rows this view computes (owned nodes)
   int64_t na;       // V block offset in the x/y layout (3 n_nodes, or 3 (L + G) on a part)
   const int* e_off = nullptr;  // NB-E: chunk slot offsets (blk / blk_col are then slot-major)
+  int64_t node_begin = 0;      // rows of nodes [node_begin, n_nodes) (split SpMV)
 };
 
 // 256-bit streaming load (read-once matrix data: no L1 allocation)
@@ -603,9 +606,10 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
 #pragma unroll
   for (int j = 0; j < NVL; ++j) part[j] = 0.0;
 
-  for (int64_t wn = warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
+  const int64_t w0 = A.node_begin & ~(int64_t)(NPW - 1);  // warps stay chunk-aligned
+  for (int64_t wn = w0 + warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
     const int64_t i = wn + lane / G;
-    const bool valid = i < A.n_nodes;
+    const bool valid = i >= A.node_begin && i < A.n_nodes;
     double2 acc[3][KL], accv[KL];
 #pragma unroll
     for (int k = 0; k < KL; ++k) {
@@ -783,7 +787,7 @@ k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   if (threadIdx.x == 0) {
     if (ctl.red) {
 #pragma unroll
-      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+      for (int j = 0; j < NV; ++j) ctl.red[j] = ctl.red_add ? ctl.red[j] + tot[j] : tot[j];
     } else if (MODE == kCocg) {
       fin_alpha<K>(ctl, tot);
     } else {
@@ -823,9 +827,10 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
 #pragma unroll
   for (int j = 0; j < NVL; ++j) part[j] = 0.0;
 
-  for (int64_t wn = warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
+  const int64_t w0 = A.node_begin & ~(int64_t)(NPW - 1);  // warps stay chunk-aligned
+  for (int64_t wn = w0 + warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
     const int64_t i = wn + lane / G;
-    const bool valid = i < A.n_nodes;
+    const bool valid = i >= A.node_begin && i < A.n_nodes;
     double2 acc[3][KL], accv[KL];
 #pragma unroll
     for (int k = 0; k < KL; ++k) {
@@ -1028,7 +1033,7 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   if (threadIdx.x == 0) {
     if (ctl.red) {
 #pragma unroll
-      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+      for (int j = 0; j < NV; ++j) ctl.red[j] = ctl.red_add ? ctl.red[j] + tot[j] : tot[j];
     } else if (MODE == kCocg) {
       fin_alpha<K>(ctl, tot);
     } else {
@@ -3079,6 +3084,26 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
   for (int64_t q = 0; q < G; ++q) g2l[H.ghost_nodes[q]] = (int)(L + q);
   DevBuf<int> d_g2l(nn);
   CK(cudaMemcpy(d_g2l.p, g2l.data(), nn * sizeof(int), cudaMemcpyHostToDevice));
+  // interior rows (no ghost column): the longest run of such owned nodes; its
+  // SpMV runs while the halo is in flight, the rest after it lands
+  {
+    int64_t best_lo = 0, best_len = 0, run_lo = 0;
+    for (int64_t i = 0; i <= L; ++i) {
+      bool boundary = i == L;
+      if (i < L)
+        for (int q = nbr_off[H.n0 + i]; q < nbr_off[H.n0 + i + 1] && !boundary; ++q)
+          boundary = g2l[nbr[q]] >= L;
+      if (boundary) {
+        if (i - run_lo > best_len) {
+          best_len = i - run_lo;
+          best_lo = run_lo;
+        }
+        run_lo = i + 1;
+      }
+    }
+    P->int_lo = best_lo;
+    P->int_hi = best_lo + best_len;
+  }
   // blocks of the owned nodes: contiguous slice of the global NB arrays
   const int64_t q0 = nbr_off[H.n0], q1 = nbr_off[H.n1];
   P->nblk = q1 - q0;
@@ -3231,7 +3256,9 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
     else if (R > 1) { k_sum_parts<<<1, 64, 0, s>>>(reds.p, R, nv); CK_LAUNCH(); }
   };
   // ghost exchange of vector v (member pointer of PartState)
-  auto halo = [&](DevBuf<double2> PartState<K>::*v) {
+  // ghost exchange of vector v; the transfers run on stream `hs_`, after the
+  // packing kernels (on s) have been recorded
+  auto halo = [&](DevBuf<double2> PartState<K>::*v, cudaStream_t hs_) {
     for (int r = 0; r < R; ++r) {
       ect_part* P = parts[r];
       for (size_t i = 0; i < P->peers.size(); ++i) {
@@ -3244,6 +3271,10 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
         CK_LAUNCH();
       }
     }
+    if (hs_ != s) {
+      CK(cudaEventRecord(ctx->ev_h1, s));
+      CK(cudaStreamWaitEvent(hs_, ctx->ev_h1, 0));
+    }
     if (comm) nccl_group_start();
     for (int r = 0; r < R; ++r) {
       ect_part* P = parts[r];
@@ -3255,10 +3286,10 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
         double2* dstV = base + (H.na_local() + H.Vo + hp.recv_v_begin) * K;
         if (comm) {
           const auto& d = P->peers[i];
-          nccl_send(comm, d.sendbuf.p, 2 * d.ns * 3 * K, hp.part, s);
-          if (d.nsc) nccl_send(comm, d.sendbuf.p + d.ns * 3 * K, 2 * d.nsc * K, hp.part, s);
-          nccl_recv(comm, dstA, 2 * hp.recv_node_count * 3 * K, hp.part, s);
-          if (hp.recv_v_count) nccl_recv(comm, dstV, 2 * hp.recv_v_count * K, hp.part, s);
+          nccl_send(comm, d.sendbuf.p, 2 * d.ns * 3 * K, hp.part, hs_);
+          if (d.nsc) nccl_send(comm, d.sendbuf.p + d.ns * 3 * K, 2 * d.nsc * K, hp.part, hs_);
+          nccl_recv(comm, dstA, 2 * hp.recv_node_count * 3 * K, hp.part, hs_);
+          if (hp.recv_v_count) nccl_recv(comm, dstV, 2 * hp.recv_v_count * K, hp.part, hs_);
         } else {
           // the owner's send buffer for this part
           ect_part* Q = parts[hp.part];
@@ -3269,26 +3300,60 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
           if (d.ns != hp.recv_node_count || d.nsc != hp.recv_v_count)
             fail(ECT_ERR_SOLVER, "halo plan: send/receive sizes differ");
           CK(cudaMemcpyAsync(dstA, d.sendbuf.p, d.ns * 3 * K * sizeof(double2),
-                             cudaMemcpyDeviceToDevice, s));
+                             cudaMemcpyDeviceToDevice, hs_));
           if (d.nsc)
             CK(cudaMemcpyAsync(dstV, d.sendbuf.p + d.ns * 3 * K, d.nsc * K * sizeof(double2),
-                               cudaMemcpyDeviceToDevice, s));
+                               cudaMemcpyDeviceToDevice, hs_));
         }
       }
     }
     if (comm) nccl_group_end();
+    if (hs_ != s) CK(cudaEventRecord(ctx->ev_h2, hs_));
+  };
+  // rows of nodes [lo, hi) of every part; add: accumulate the dot totals
+  auto spmv_rows = [&](int mode, DevBuf<double2> PartState<K>::*xin,
+                       DevBuf<double2> PartState<K>::*yout, bool with_b, int64_t lo, int64_t hi,
+                       bool add, int r) {
+    NbView v = part_view(parts[r]);
+    v.node_begin = lo;
+    v.n_nodes = hi;
+    const double2* xp = (S[r].*xin).p;
+    double2* yp = (S[r].*yout).p;
+    const double2* bp = with_b ? S[r].b.p : nullptr;
+    KrylovCtl c = S[r].ctl;
+    c.red_add = add ? 1 : 0;
+    void* args[] = {&v, &xp, &yp, &bp, &c};
+    CK(cudaLaunchKernel(part_fn<K>(parts[r], ctx->nb_variant, mode), dim3(grid_s), dim3(kBlock),
+                        args, 0, s));
   };
   auto spmv = [&](int mode, DevBuf<double2> PartState<K>::*xin, DevBuf<double2> PartState<K>::*yout,
                   bool with_b) {
+    for (int r = 0; r < R; ++r)
+      spmv_rows(mode, xin, yout, with_b, 0, parts[r]->plan.L, false, r);
+  };
+  // q = A p with the halo exchange overlapped: interior rows while the ghost
+  // values travel (halo stream), then the rows that read ghosts
+  const bool overlap = true;  // halo transfers on their own stream
+  if (!ctx->halo_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->halo_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_h1, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_h2, cudaEventDisableTiming));
+  }
+  auto spmv_overlapped = [&](DevBuf<double2> PartState<K>::*xin,
+                             DevBuf<double2> PartState<K>::*yout) {
+    halo(xin, overlap ? ctx->halo_stream : s);
     for (int r = 0; r < R; ++r) {
-      NbView v = part_view(parts[r]);
-      const double2* xp = (S[r].*xin).p;
-      double2* yp = (S[r].*yout).p;
-      const double2* bp = with_b ? S[r].b.p : nullptr;
-      KrylovCtl c = S[r].ctl;
-      void* args[] = {&v, &xp, &yp, &bp, &c};
-      CK(cudaLaunchKernel(part_fn<K>(parts[r], ctx->nb_variant, mode), dim3(grid_s), dim3(kBlock),
-                          args, 0, s));
+      const ect_part* P = parts[r];
+      if (P->int_hi > P->int_lo) spmv_rows(kCocg, xin, yout, false, P->int_lo, P->int_hi, false, r);
+    }
+    if (overlap) CK(cudaStreamWaitEvent(s, ctx->ev_h2, 0));
+    for (int r = 0; r < R; ++r) {
+      const ect_part* P = parts[r];
+      const bool any = P->int_hi > P->int_lo;
+      if (P->int_lo > 0) spmv_rows(kCocg, xin, yout, false, 0, P->int_lo, any, r);
+      if (P->int_hi < P->plan.L)
+        spmv_rows(kCocg, xin, yout, false, any ? P->int_hi : P->int_lo, P->plan.L,
+                  any || P->int_lo > 0, r);
     }
   };
   auto fin = [&](int what, unsigned mask, int fresh) {
@@ -3322,8 +3387,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
   for (int round = 0;; ++round) {
     for (int launched = 0; opt.max_iter > 0 && launched <= opt.max_iter + chunk;) {
       for (int it = 0; it < chunk; ++it) {
-        halo(&PartState<K>::p);
-        spmv(kCocg, &PartState<K>::p, &PartState<K>::q, false);
+        spmv_overlapped(&PartState<K>::p, &PartState<K>::q);
         allreduce(2 * K);
         fin(kFinAlpha, 0, 0);
         for (int r = 0; r < R; ++r)
@@ -3352,7 +3416,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
       }
       CK(cudaStreamSynchronize(s));
     }
-    halo(&PartState<K>::x);
+    halo(&PartState<K>::x, s);
     spmv(kResid, &PartState<K>::x, &PartState<K>::q, true);
     allreduce(K);
     fin(kFinResid, 0, 0);
