@@ -2095,7 +2095,7 @@ size_t nbs_bytes(const NbsCfg& c, ect_matrix* a, int mode) {
 template <int K>
 struct Dispatch {
   static constexpr int kWidth = K;
-  static constexpr bool kNbOk = K <= 8;
+  static constexpr bool kNbOk = K <= 16;
   static constexpr bool kNbtOk = K <= 4;
   static bool use_nbt(const ect_matrix* a) {
     return kNbtOk && a->has_nbt && nbt_smem<K>(a) <= kNbtMaxSmem;
