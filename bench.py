@@ -247,7 +247,10 @@ def run_ours(args):
                                    if nb["format"] != "csr" else f"k_spmv (CSR, k={k})",
                          "mean_launch_ms": spmv_ms,
                          "launches_timed": int(tm["spmv_launches"]),
-                         "launch_sampling": "CUDA events on every 8th solver iteration",
+                         "launch_sampling": "CUDA events on every 8th solver iteration; only "
+                                            "iterations with all k columns still active "
+                                            f"({int(tm['spmv_partial_launches'])} partial-width "
+                                            "samples excluded)",
                          "algorithmic_bytes": b_spmv,
                          "algorithmic_bytes_note": "SURVEY 8(d) CSR formula 20*nnz+4*(N+1)+32*k*N; "
                                                    "NB stores the same matrix in fewer bytes",
@@ -330,13 +333,17 @@ def cpu_baseline_leg(a, mesh, w, positions, threads):
                                        threads=nthreads)
         its = int(out["iterations"].sum())
         # the reference's CscMatrix::multiply, single thread
-        xs = np.ascontiguousarray(b[:, 0])
+        # dense x as configs[2] (re, im uniform [-1, 1], seed 2): the reference
+        # skips x_j = 0 (sparse.cpp:115-124), so a coil RHS would time mostly zeros
+        rng = np.random.default_rng(2)
+        xs = rng.uniform(-1, 1, a.n) + 1j * rng.uniform(-1, 1, a.n)
         _, t_mv = rs.multiply(xs, repeat=3)
         b_mv = 20 * a.nnz + 4 * (a.n + 1) + 32 * a.n
         return {"value": a.n * its / out["seconds"], "unit": UNIT, "cores": nthreads,
                 "kind": "reference",
                 "spmv_single_thread_GBps": b_mv / (t_mv / 3) / 1e9,
                 "spmv_single_thread_ms": t_mv / 3 * 1e3,
+                "spmv_sample": "CscMatrix::multiply x3, dense seeded x (configs[2] distribution)",
                 "sample": f"{nthreads} concurrent solve_iterative calls (GMRES(80)+ILU(0), "
                           f"ILU rebuilt per call as iterative.cpp:126) x {max_iter} iterations "
                           f"on the configs[1] primary matrix; {out['seconds']:.1f} s wall"}

@@ -120,11 +120,17 @@ typedef struct ect_timings {
   double assemble_ms;
   double rhs_ms;
   double solve_ms;
+  /* Sampled solver kernels (ect_ctx_set_profiling): only iterations in which
+   * EVERY column of the batch was still active are summed here, so that a
+   * duration matches the full-width algorithmic bytes; samples taken after some
+   * columns converged (cheaper launches) are counted in *_partial_launches. */
   double spmv_ms_total;   /* sum of SpMV kernel durations inside the solve */
   int64_t spmv_launches;
   int64_t kernel_launches;
   double vec_ms_total;    /* fused vector-update kernels (update + p-update) */
   int64_t vec_launches;
+  int64_t spmv_partial_launches;
+  int64_t vec_partial_launches;
 } ect_timings;
 
 /* ---- context --------------------------------------------------------- */

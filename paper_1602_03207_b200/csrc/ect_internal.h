@@ -73,6 +73,8 @@ struct RhsState {
   double rnorm;
   int iters;
   int status;     // kActive / kConverged / kBreakdown / kMaxIter / kZeroRhs
+  int xpend;      // COCG: x += alpha p still owed (applied by the next p-update)
+  int pad_;
 };
 enum RhsStatus : int { kActive = 0, kConverged = 1, kBreakdown = 2, kMaxIter = 3, kZeroRhs = 4 };
 
@@ -81,6 +83,11 @@ struct Profile {
   bool enabled = false;
   std::vector<cudaEvent_t> pool;  // pairs (start, stop)
   std::vector<int> kinds;          // kind of the pair starting at index i
+  // solver samples: the batch width and the slot of `snaps` holding the
+  // device-side active-column count at the sampled iteration (-1: none)
+  std::vector<int> widths, snap_of;
+  DevBuf<int> snaps;
+  size_t n_snaps = 0;
   size_t used = 0;
   int64_t launches = 0;
 };

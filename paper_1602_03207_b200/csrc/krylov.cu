@@ -190,6 +190,7 @@ __device__ void fin_update(const KrylovCtl& ctl, const double* tot) {
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     RhsState& s = ctl.st[k];
+    s.xpend = s.status == kActive;  // this iteration's x += alpha p is owed to k_pupdate
     if (s.status != kActive) continue;
     const double2 rho_new = make_double2(tot[3 * k], tot[3 * k + 1]);
     s.rnorm = sqrt(tot[3 * k + 2]);
@@ -854,26 +855,32 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       }
       // (wide per-lane batches keep the accumulators instead)
       constexpr bool kPipe = KL <= 2 && MINB <= 2;
+      // L2 prefetch of the warp's block rows PFD steps ahead: the DRAM latency
+      // of the matrix stream is covered without holding registers. Lanes
+      // 0 .. 3 LINES - 1 own one 128-B line of a plane row, lane 3 LINES the
+      // column row; the line address of row r is pf + r * stride.
+      constexpr int LINES = NPW >= 4 ? NPW / 4 : 1;  // 128-B lines per plane row
+      const char* pf = nullptr;
+      int pf_stride = 0;
+      if constexpr (PFD > 0) {
+        if (lane < 3 * LINES) {
+          pf = reinterpret_cast<const char*>(A.blk + 4 * ((int64_t)(lane / LINES) * A.nblk + o32 +
+                                                          (int)(wn & 31)) +
+                                             16 * (lane % LINES));
+          pf_stride = 32 * 32;  // 32 slots x 4 doubles
+        } else if (lane == 3 * LINES) {
+          pf = reinterpret_cast<const char*>(A.blk_col + o32 + (int)(wn & 31));
+          pf_stride = 32 * 4;
+        }
+      }
       for (; q < be; q += GS) {
         if constexpr (PFD > 0) {
-          // L2 prefetch of the warp's block rows PFD steps ahead: the DRAM
-          // latency of the matrix stream is covered without holding registers
-          constexpr int LINES = NPW >= 4 ? NPW / 4 : 1;  // 128-B lines per plane row
-          const int row0 = (((q - sbase) >> 5) - bl + PFD * GB);
-          if (lane < 3 * LINES + 1) {
+          const int row0 = ((q - sbase) >> 5) - bl + PFD * GB;
+          if (pf) {
 #pragma unroll
-            for (int gb = 0; gb < GB; ++gb) {
-              const int jrow = row0 + gb;
-              if (jrow < w32) {
-                const int64_t wslot = o32 + (int)(wn & 31) + 32 * (int64_t)jrow;
-                const void* pa =
-                    lane < 3 * LINES
-                        ? (const void*)(A.blk + 4 * ((int64_t)(lane / LINES) * A.nblk + wslot) +
-                                        16 * (lane % LINES))
-                        : (const void*)(A.blk_col + wslot);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
-              }
-            }
+            for (int gb = 0; gb < GB; ++gb)
+              if (row0 + gb < w32)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)(row0 + gb) * pf_stride));
           }
         }
         int m = m_nx;
@@ -1745,12 +1752,13 @@ struct VecMap {
   static constexpr int KH = K / CW;
 };
 
-// x += alpha p ; r -= alpha q ; z = D^-1 r ; partial r^T z, ||r||^2
-// last block: convergence test, beta, rho.
+// r -= alpha q ; z = D^-1 r ; partial r^T z, ||r||^2
+// last block: convergence test, beta, rho. The iteration's x += alpha p is
+// deferred to k_pupdate, which reads p anyway (x and p travel once, not twice).
 template <int K>
 __global__ void __launch_bounds__(kBlock)
-k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const double2* __restrict__ p,
-         const double2* __restrict__ q, const double2* __restrict__ dinv, KrylovCtl ctl) {
+k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
+         const double2* __restrict__ dinv, KrylovCtl ctl) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
   constexpr int NVL = 3 * CW, NV = 3 * K;
   __shared__ double smem[32 * NV];
@@ -1776,11 +1784,7 @@ k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const doub
     for (int c = 0; c < CW; ++c) {
       if (!act[c]) continue;
       const int64_t idx = i * K + kb + c;
-      const double2 pv = p[idx], qv = q[idx];
-      double2 xv = x[idx], rv = r[idx];
-      xv = cadd(xv, cmul(alpha[c], pv));
-      rv = csub(rv, cmul(alpha[c], qv));
-      x[idx] = xv;
+      const double2 rv = csub(r[idx], cmul(alpha[c], q[idx]));
       r[idx] = rv;
       const double2 z = cmul(d, rv);
       part[3 * c] += rv.x * z.x - rv.y * z.y;
@@ -1807,20 +1811,26 @@ k_update(int64_t n, double2* __restrict__ x, double2* __restrict__ r, const doub
   }
 }
 
-// p = D^-1 r + beta p
+// x += alpha p (owed by the last k_update) ; p = D^-1 r + beta p (active columns)
 template <int K>
 __global__ void __launch_bounds__(kBlock)
-k_pupdate(int64_t n, const double2* __restrict__ r, double2* __restrict__ p,
-          const double2* __restrict__ dinv, KrylovCtl ctl) {
+k_pupdate(int64_t n, double2* __restrict__ x, const double2* __restrict__ r,
+          double2* __restrict__ p, const double2* __restrict__ dinv, KrylovCtl ctl) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
-  if (*ctl.n_active == 0) return;
+  bool any = *ctl.n_active != 0;
+#pragma unroll
+  for (int c = 0; c < K; ++c) any |= ctl.st[c].xpend != 0;
+  if (!any) return;
   const int h = (threadIdx.x & 31) % KH, kb = h * CW;
-  bool act[CW];
-  double2 beta[CW];
+  bool act[CW], xp[CW];
+  double2 alpha[CW], beta[CW];
 #pragma unroll
   for (int c = 0; c < CW; ++c) {
-    act[c] = ctl.st[kb + c].status == kActive;
-    beta[c] = ctl.st[kb + c].beta;
+    const RhsState& st = ctl.st[kb + c];
+    act[c] = st.status == kActive;
+    xp[c] = st.xpend != 0;
+    alpha[c] = st.alpha;
+    beta[c] = st.beta;
   }
   const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
@@ -1830,10 +1840,19 @@ k_pupdate(int64_t n, const double2* __restrict__ r, double2* __restrict__ p,
     const double2 d = dinv[i];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
-      if (!act[c]) continue;
+      if (!act[c] && !xp[c]) continue;
       const int64_t idx = i * K + kb + c;
-      p[idx] = cadd(cmul(d, r[idx]), cmul(beta[c], p[idx]));
+      const double2 pv = p[idx];
+      if (xp[c]) x[idx] = cadd(x[idx], cmul(alpha[c], pv));
+      if (act[c]) p[idx] = cadd(cmul(d, r[idx]), cmul(beta[c], pv));
     }
+  }
+  // the owed updates are done: clear the flags (after every block read them)
+  if (!last_block(ctl.counter)) return;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) ctl.st[c].xpend = 0;
+    *ctl.counter = 0u;
   }
 }
 
@@ -2165,14 +2184,14 @@ struct Dispatch {
       k_spmv<G, K, kResid><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
     CK_LAUNCH();
   }
-  static void update(ect_ctx* ctx, int grid, int64_t n, double2* x, double2* r, const double2* p,
-                     const double2* q, const double2* dinv, KrylovCtl ctl) {
-    k_update<K><<<grid, kBlock, 0, ctx->stream>>>(n, x, r, p, q, dinv, ctl);
+  static void update(ect_ctx* ctx, int grid, int64_t n, double2* r, const double2* q,
+                     const double2* dinv, KrylovCtl ctl) {
+    k_update<K><<<grid, kBlock, 0, ctx->stream>>>(n, r, q, dinv, ctl);
     CK_LAUNCH();
   }
-  static void pupdate(ect_ctx* ctx, int grid, int64_t n, const double2* r, double2* p,
+  static void pupdate(ect_ctx* ctx, int grid, int64_t n, double2* x, const double2* r, double2* p,
                       const double2* dinv, KrylovCtl ctl) {
-    k_pupdate<K><<<grid, kBlock, 0, ctx->stream>>>(n, r, p, dinv, ctl);
+    k_pupdate<K><<<grid, kBlock, 0, ctx->stream>>>(n, x, r, p, dinv, ctl);
     CK_LAUNCH();
   }
   static void start(ect_ctx* ctx, int grid, int64_t n, const double2* b, double2* x, double2* r,
@@ -2234,11 +2253,16 @@ void with_k(int k, F&& fn) {
 // sampled = true (solver loop): time one launch in kProfStride, so the event
 // records do not perturb the timed region; the mean is over the sampled ones.
 constexpr int kProfStride = 8;
-void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0, bool sampled = false) {
+void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0, bool sampled = false,
+                const int* n_active = nullptr, int width = 0, int snap = -1) {
   ev[0] = ev[1] = nullptr;
   if (!ctx->prof.enabled) return;
   auto& P = ctx->prof;
-  if (sampled && (P.launches++ % kProfStride) != 0) return;
+  static const int stride = [] {
+    const char* v = std::getenv("ECT_PROF_STRIDE");  // dev: sample every n-th iteration
+    return v ? std::max(1, std::atoi(v)) : kProfStride;
+  }();
+  if (sampled && (P.launches++ % stride) != 0) return;
   if (P.used + 2 > P.pool.size()) {
     for (int i = 0; i < 512; ++i) {
       cudaEvent_t e;
@@ -2247,7 +2271,25 @@ void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0, bool sampled = fals
     }
   }
   P.kinds.resize(P.pool.size());
+  P.widths.resize(P.pool.size());
+  P.snap_of.resize(P.pool.size());
   P.kinds[P.used] = kind;
+  P.widths[P.used] = width;
+  P.snap_of[P.used] = snap;
+  if (n_active) {  // snapshot the active-column count this launch will see
+    if (P.n_snaps + 1 > P.snaps.n) {
+      DevBuf<int> grown(std::max<size_t>(1024, 2 * P.snaps.n));
+      if (P.n_snaps)
+        CK(cudaMemcpyAsync(grown.p, P.snaps.p, P.n_snaps * sizeof(int), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      P.snaps = std::move(grown);
+    }
+    P.snap_of[P.used] = (int)P.n_snaps;
+    CK(cudaMemcpyAsync(P.snaps.p + P.n_snaps, n_active, sizeof(int), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    ++P.n_snaps;
+  }
   ev[0] = P.pool[P.used++];
   ev[1] = P.pool[P.used++];
   CK(cudaEventRecord(ev[0], ctx->stream));
@@ -2256,22 +2298,43 @@ void prof_end(ect_ctx* ctx, cudaEvent_t* ev) {
   if (!ctx->prof.enabled || ev[0] == nullptr) return;
   CK(cudaEventRecord(ev[1], ctx->stream));
 }
+// slot of the snapshot taken by the pair whose start event is ev0 (-1 if none)
+int prof_snap_of(ect_ctx* ctx, cudaEvent_t ev0) {
+  auto& P = ctx->prof;
+  for (size_t i = P.used; i >= 2; i -= 2)
+    if (P.pool[i - 2] == ev0) return P.snap_of[i - 2];
+  return -1;
+}
 void prof_collect(ect_ctx* ctx) {
   auto& P = ctx->prof;
   if (!P.enabled || P.used == 0) return;
   CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<int> act(P.n_snaps);
+  if (P.n_snaps)
+    CK(cudaMemcpy(act.data(), P.snaps.p, P.n_snaps * sizeof(int), cudaMemcpyDeviceToHost));
   for (size_t i = 0; i + 1 < P.used; i += 2) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, P.pool[i], P.pool[i + 1]));
+    // a solver sample counts only if all `width` columns were active
+    const bool full = P.snap_of[i] < 0 || act[(size_t)P.snap_of[i]] >= P.widths[i];
     if (P.kinds[i] == 0) {
-      ctx->timings.spmv_ms_total += ms;
-      ctx->timings.spmv_launches += 1;
+      if (full) {
+        ctx->timings.spmv_ms_total += ms;
+        ctx->timings.spmv_launches += 1;
+      } else {
+        ctx->timings.spmv_partial_launches += 1;
+      }
     } else {
-      ctx->timings.vec_ms_total += ms;
-      ctx->timings.vec_launches += 1;
+      if (full) {
+        ctx->timings.vec_ms_total += ms;
+        ctx->timings.vec_launches += 1;
+      } else {
+        ctx->timings.vec_partial_launches += 1;
+      }
     }
   }
   P.used = 0;
+  P.n_snaps = 0;
 }
 
 }  // namespace
@@ -2909,14 +2972,15 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       for (; opt.max_iter > 0;) {
         for (int it = 0; it < chunk; ++it) {
           cudaEvent_t ev[2];
-          prof_begin(ctx, ev, 0, true);
+          prof_begin(ctx, ev, 0, true, n_active.p, k);
           DK::spmv(ctx, kCocg, grid_s, n, a, p.p, q.p, nullptr, ctl);
           prof_end(ctx, ev);
           cudaEvent_t ev2[2];
           ev2[0] = ev2[1] = nullptr;
-          if (ev[0]) prof_begin(ctx, ev2, 1);  // same sampled iterations as the SpMV
-          DK::update(ctx, grid_v, n, xx.p, r.p, p.p, q.p, a->dinv.p, ctl);
-          DK::pupdate(ctx, grid_v, n, r.p, p.p, a->dinv.p, ctl);
+          // same sampled iterations as the SpMV, same active-column snapshot
+          if (ev[0]) prof_begin(ctx, ev2, 1, false, nullptr, k, prof_snap_of(ctx, ev[0]));
+          DK::update(ctx, grid_v, n, r.p, q.p, a->dinv.p, ctl);
+          DK::pupdate(ctx, grid_v, n, xx.p, r.p, p.p, a->dinv.p, ctl);
           prof_end(ctx, ev2);
           note_launch(ctx, 3);
         }
@@ -3391,13 +3455,13 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
         allreduce(2 * K);
         fin(kFinAlpha, 0, 0);
         for (int r = 0; r < R; ++r)
-          DK::update(ctx, grid_v, parts[r]->plan.n_local(), S[r].x.p, S[r].r.p, S[r].p.p,
-                     S[r].q.p, parts[r]->dinv.p, S[r].ctl);
+          DK::update(ctx, grid_v, parts[r]->plan.n_local(), S[r].r.p, S[r].q.p,
+                     parts[r]->dinv.p, S[r].ctl);
         allreduce(3 * K);
         fin(kFinUpdate, 0, 0);
         for (int r = 0; r < R; ++r)
-          DK::pupdate(ctx, grid_v, parts[r]->plan.n_local(), S[r].r.p, S[r].p.p, parts[r]->dinv.p,
-                      S[r].ctl);
+          DK::pupdate(ctx, grid_v, parts[r]->plan.n_local(), S[r].x.p, S[r].r.p, S[r].p.p,
+                      parts[r]->dinv.p, S[r].ctl);
       }
       launched += chunk;
       CK(cudaMemcpyAsync(flag, S[0].n_active.p, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -82,7 +82,8 @@ class SignalPoint(C.Structure):
 class Timings(C.Structure):
     _fields_ = [("pattern_ms", D), ("assemble_ms", D), ("rhs_ms", D), ("solve_ms", D),
                 ("spmv_ms_total", D), ("spmv_launches", I64), ("kernel_launches", I64),
-                ("vec_ms_total", D), ("vec_launches", I64)]
+                ("vec_ms_total", D), ("vec_launches", I64),
+                ("spmv_partial_launches", I64), ("vec_partial_launches", I64)]
 
 
 _lib = None
@@ -189,9 +190,9 @@ class Mesh:
         g = read_gmsh(path)
         return cls(ctx, g["xyz"], g["tets"], g["region"])
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None):
-            lib().ect_mesh_destroy(self.h)
+            _lib().ect_mesh_destroy(self.h)
             self.h = None
 
     def export(self):
@@ -248,9 +249,9 @@ class Matrix:
         _check(lib().ect_matrix_counts(h, C.byref(n), C.byref(nnz)))
         self.n, self.nnz = n.value, nnz.value
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None) and not getattr(self, "_borrowed", False):
-            lib().ect_matrix_destroy(self.h)
+            _lib().ect_matrix_destroy(self.h)
             self.h = None
 
     def assemble(self, mats: Materials):
@@ -319,9 +320,9 @@ class Session:
                                         C.byref(opts), C.byref(h)))
         self.h = h
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None):
-            lib().ect_session_destroy(self.h)
+            _lib().ect_session_destroy(self.h)
             self.h = None
 
     def matrix(self, reference=False) -> Matrix:
@@ -411,9 +412,9 @@ class HaloPlan:
                                "recv_v_begin": pi[3], "recv_v_count": pi[4],
                                "send_nodes": sn, "send_cond_nodes": sc})
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None):
-            lib().ect_halo_plan_destroy(self.h)
+            _lib().ect_halo_plan_destroy(self.h)
             self.h = None
 
 
@@ -432,9 +433,9 @@ class Comm:
         _check(lib().ect_comm_create(ctx.h, I32(rank), I32(world), buf, C.byref(h)))
         self.h = h
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None):
-            lib().ect_comm_destroy(self.h)
+            _lib().ect_comm_destroy(self.h)
             self.h = None
 
 
@@ -451,9 +452,9 @@ class Part:
         _check(lib().ect_part_info(h, info))
         self.info = dict(zip(["n0", "n1", "L", "G", "Vo", "Vg", "n_peers", "n_blocks"], list(info)))
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None):
-            lib().ect_part_destroy(self.h)
+            _lib().ect_part_destroy(self.h)
             self.h = None
 
 

@@ -1,8 +1,11 @@
 """Summarise an ncu capture of the SpMV kernel + a launch list into the JSON
 bench.py reads for roofline.traffic (profiles/spmv_ncu_summary.json).
 
-  python scripts/ncu_summary.py REPORT.ncu-rep LAUNCHES.csv OUT.json \
+  python scripts/ncu_summary.py REPORT.ncu-rep|RAW.csv LAUNCHES.csv OUT.json \
       --command "..." --capture "..." --format-bytes B
+
+REPORT may also be the `ncu -i REPORT --page raw --csv` export (made on the GPU
+box, where the report itself is too large to bring back).
 """
 import argparse
 import csv
@@ -19,8 +22,11 @@ KEEP = ["sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_
 
 
 def raw(report):
-    out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if report.endswith(".csv"):
+        out = open(report).read()
+    else:
+        out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2]
 
