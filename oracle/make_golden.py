@@ -13,8 +13,14 @@ check parity against committed data:
                  right-hand sides and GMRES(80)+ILU(0) solutions at tol 1e-12.
   cfg1.json      configs[1]: counts + sha256 of the CSC pattern and values
                  (reference assembly takes minutes and ~20 GB; run once).
+  cfg3_point.json one configs[3] probe position on the configs[1] mesh (the
+                 coil pair next to the deposit): the reference's solve_position
+                 chain -- both material configurations assembled (parts = 1),
+                 position_rhs for both coils, solve_iterative (GMRES(80)+ILU(0))
+                 at a tight tolerance, delta_impedance x4 and signal_modes.
+                 Hours of single-threaded CPU; run once.
 
-usage: python -m oracle.make_golden [small|cfg0|cfg1|all]
+usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|all]
 """
 from __future__ import annotations
 
@@ -148,6 +154,44 @@ def make_cfg1():
     (GOLDEN / "cfg1.json").write_text(json.dumps(out, indent=1))
 
 
+CFG3_INDEX = 31    # configs[3] position 31 of 64: z = 0.989 cm, the coil pair at the deposit
+CFG3_TOL = 1e-11
+
+
+def make_cfg3_point():
+    """ScanSession::solve_position (scan.cpp:95-143) at one configs[3] position
+    on the full configs[1] mesh, through the unmodified reference."""
+    w = workloads.config3()
+    z = w.positions[CFG3_INDEX]
+    t0 = time.time()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    assert two
+    xs, info = {}, {}
+    for tag, mats in (("primary", prim), ("reference", refm)):
+        s = ref.RefSystem(rm, mats, parts=1, workers=1)
+        b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for c in (1, 2)])
+        out = s.solve_iterative_batch(b, tol=CFG3_TOL, max_iter=200000, restart=80, threads=2,
+                                      want_x=True)
+        res = [s.relative_residual(out["x"][c], b[c]) for c in range(2)]
+        assert max(res) <= CFG3_TOL * 1.01, res
+        xs[tag] = out["x"]
+        info[tag] = {"iterations": [int(i) for i in out["iterations"]], "true_residual": res,
+                     "solve_s": out["seconds"]}
+        print(tag, info[tag], f"{time.time() - t0:.0f}s", flush=True)
+        del s
+    dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][k], xs["reference"][l])
+                   for k in range(2) for l in range(2)])
+    modes = ref.signal_modes(dz)
+    doc = {"position_index": CFG3_INDEX, "z": z, "tol": CFG3_TOL, "solver": "GMRES(80)+ILU(0)",
+           "dz": [[v.real, v.imag] for v in dz],
+           "modes": [[complex(v).real, complex(v).imag] for v in modes], **info,
+           "wall_s": time.time() - t0}
+    (GOLDEN / "cfg3_point.json").write_text(json.dumps(doc, indent=1))
+    print("cfg3 point written", doc, flush=True)
+
+
 TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
 
 
@@ -249,6 +293,8 @@ if __name__ == "__main__":
         make_small()
     if what in ("cfg0", "all"):
         make_cfg0()
+    if what in ("cfg3",):
+        make_cfg3_point()
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):

@@ -95,3 +95,29 @@ def test_cfg1_bit_exact_and_solve_properties(ctx):
     assert res[0]["converged"]
     rr = np.linalg.norm(b - A @ x) / np.linalg.norm(b)
     assert rr <= 1e-8 * 1.01, rr
+
+
+def test_cfg3_point_impedance_matches_reference(ctx):
+    """configs[3] on the full configs[1] mesh: ScanSession::solve_position at
+    the position next to the deposit vs the unmodified reference chain
+    (tests/golden/cfg3_point.json: both configurations assembled with
+    parts = 1, GMRES(80)+ILU(0) to the same tight tolerance, delta_impedance
+    x4, signal_modes). Bar: |dZ - dZ*| / max|dZ*| <= 1e-6, same for Z_FA/Z_F3."""
+    path = GOLDEN / "cfg3_point.json"
+    if not path.exists():
+        pytest.skip("cfg3_point.json not generated (python -m oracle.make_golden cfg3)")
+    gold = json.loads(path.read_text())
+    w = workloads.config3()
+    assert w.positions[gold["position_index"]] == gold["z"]
+    m = w.mesh()
+    mesh = ect.Mesh(ctx, m.xyz, m.tets, m.region)
+    s = ect.Session(ctx, mesh, w.physics, w.coil, w.amplitude, tol=gold["tol"], max_iter=200000)
+    pt = s.solve_positions([gold["z"]])[0]
+    assert not pt["failed"]
+    dz_ref = np.array([complex(*v) for v in gold["dz"]])
+    scale = np.max(np.abs(dz_ref))
+    err = np.max(np.abs(pt["dz"] - dz_ref)) / scale
+    assert err <= 1e-6, err
+    fa, f3 = (complex(*v) for v in gold["modes"])
+    mscale = max(abs(fa), abs(f3))
+    assert abs(pt["z_fa"] - fa) / mscale <= 1e-6 and abs(pt["z_f3"] - f3) / mscale <= 1e-6
