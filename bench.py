@@ -447,7 +447,8 @@ def run_micro(args):
 
 
 def run_large(args):
-    """configs[4]: one 27.4M-DOF system, rows partitioned by slabs of i-planes
+    """configs[4]: one 27.4M-DOF system, rows partitioned by z-slabs (the mesh is
+    numbered z-slowest, so contiguous node ranges are slabs of z-planes)
     over the GPUs (NCCL halo per SpMV + allreduce per dot), strong scaling."""
     world, rank, local = dist_env()
     import torch
@@ -500,7 +501,7 @@ def run_large(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded jittered Kuhn box, BASELINE configs[4])",
             "config": {"workload": "configs[4] 128x128x512 (50.3M tets, N=%d), coil pair at z=1 cm, "
-                                   "rows split in slabs of i-planes" % N,
+                                   "rows split in z-slabs (nodes numbered z-slowest)" % N,
                        "parallelism": f"row partition over {world} GPU(s), NCCL halo + allreduce",
                        "krylov_iterations_timed": iters, "part": part.info},
             "clocks": clk.summary(),

@@ -79,8 +79,18 @@ def centroids(xyz: np.ndarray, tets: np.ndarray) -> np.ndarray:
 
 def kuhn_box(nx: int, ny: int, nz: int, *, extent=(1.0, 1.0, 2.0), seed: int | None = 0,
              jitter: float = 0.1, origin=(0.2, 0.5), scale: float = 0.01,
-             slab=(0.4, 0.6), deposits=((0.9, 1.1),), tsp_deposits=()) -> BoxMesh:
-    """Jittered Kuhn box; see module docstring for the conventions."""
+             slab=(0.4, 0.6), deposits=((0.9, 1.1),), tsp_deposits=(),
+             node_order: str = "ijk") -> BoxMesh:
+    """Jittered Kuhn box; see module docstring for the conventions.
+
+    node_order "ijk" (default) numbers nodes (i*(ny+1)+j)*(nz+1)+k as the
+    reference's unit_cube_mesh does; "kij" renumbers the SAME geometry and tets
+    as (k*(nx+1)+i)*(ny+1)+j, so that contiguous node ranges are z-slabs (the
+    row partition of configs[4]). Geometry, tet order and orientation are
+    identical; only the labels change (the reference numbers DOFs by node id,
+    so its matrix for the relabelled mesh is P A P^T)."""
+    if node_order not in ("ijk", "kij"):
+        raise ValueError(f"node_order must be 'ijk' or 'kij', got {node_order!r}")
     lx, ly, lz = extent
     hx, hy, hz = lx / nx, ly / ny, lz / nz
     i = np.arange(nx + 1, dtype=np.int64)
@@ -132,6 +142,12 @@ def kuhn_box(nx: int, ny: int, nz: int, *, extent=(1.0, 1.0, 2.0), seed: int | N
     for z0, z1 in tsp_deposits:
         region[in_slab & (c[:, 2] >= z0) & (c[:, 2] <= z1)] = TSP
 
+    if node_order == "kij":
+        new_id = ((kk * (nx + 1) + ii) * (ny + 1) + jj).ravel()  # indexed by the ijk id
+        xyz_k = np.empty_like(xyz)
+        xyz_k[new_id] = xyz
+        xyz, tets = xyz_k, new_id[tets]
+
     xyz_m = np.empty_like(xyz)
     xyz_m[:, 0] = (xyz[:, 0] - origin[0]) * scale
     xyz_m[:, 1] = (xyz[:, 1] - origin[1]) * scale
@@ -140,4 +156,4 @@ def kuhn_box(nx: int, ny: int, nz: int, *, extent=(1.0, 1.0, 2.0), seed: int | N
                    region=region, dims=(nx, ny, nz), extent=tuple(extent),
                    origin=tuple(origin), scale=scale,
                    meta={"seed": seed, "jitter": jitter, "slab": slab, "deposits": deposits,
-                         "h": (hx, hy, hz)})
+                         "h": (hx, hy, hz), "node_order": node_order})

@@ -63,7 +63,8 @@ class Workload:
     def mesh(self) -> BoxMesh:
         return kuhn_box(*self.dims, extent=self.extent, seed=self.seed, origin=COIL_AXIS,
                         scale=SCALE, deposits=self.deposits,
-                        tsp_deposits=self.extra.get("tsp_deposits", ()))
+                        tsp_deposits=self.extra.get("tsp_deposits", ()),
+                        node_order=self.extra.get("node_order", "ijk"))
 
 
 def _coil(nz: int, lz: float = 2.0) -> tuple:
@@ -99,12 +100,14 @@ def config3() -> Workload:
 def config4() -> Workload:
     """configs[4]: 128x128x512 cells (50.3M tets) on a [0,1]x[0,1]x[0,4] box so
     that h_z = h_x and the second deposit z in [2.5, 2.7] lies inside (SURVEY
-    §8(d)); second deposit sigma = 5e3, mu_r = 2 via the TSP tag."""
+    §8(d)); second deposit sigma = 5e3, mu_r = 2 via the TSP tag. Nodes are
+    numbered z-slowest (node_order "kij") so that the contiguous node ranges of
+    the row partition are the z-slabs BASELINE asks for."""
     return Workload("configs[4]", (128, 128, 512), 3, ((0.9, 1.1),),
                     Physics(sigma_defect=1e4, mu_r_defect=5.0, sigma_tsp=5e3, mu_r_tsp=2.0),
                     _coil(512, 4.0), 1e6, (1.0 * SCALE,), extent=(1.0, 1.0, 4.0),
-                    notes="large mesh (single-GPU run; the z-slab split is round 2)",
-                    extra={"tsp_deposits": ((2.5, 2.7),)})
+                    notes="large mesh, z-slab row partition",
+                    extra={"tsp_deposits": ((2.5, 2.7),), "node_order": "kij"})
 
 
 def small(n=(4, 4, 8), seed=7, deposit=True) -> Workload:

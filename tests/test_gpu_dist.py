@@ -67,3 +67,40 @@ def test_nccl_transport_single_rank(ctx):
     for c in range(2):
         assert rd[c]["converged"]
         assert np.linalg.norm(xd[:, c] - x1[:, c]) <= 1e-8 * np.linalg.norm(x1[:, c])
+
+
+def test_zslab_partition_of_relabelled_configs0(ctx):
+    """configs[4]'s layout at configs[0] size: the mesh numbered z-slowest, cut
+    into 4 contiguous node ranges = z-slabs; the partitioned solve, mapped back
+    to the reference numbering, matches the reference's GMRES solution."""
+    w = workloads.config0()
+    ref_mesh = w.mesh()
+    w.extra = dict(w.extra, node_order="kij")
+    mm = w.mesh()
+    m = ect.Mesh(ctx, mm.xyz, mm.tets, mm.region)
+    p, _, _ = m.materials(w.physics)
+    a = ect.Matrix(ctx, m).assemble(p)
+    nx, ny, nz = w.dims
+    ii, jj, kk = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
+    new_id = ((kk * (nx + 1) + ii) * (ny + 1) + jj).ravel()  # reference node -> relabelled node
+    assert np.array_equal(new_id[ref_mesh.tets], mm.tets)
+    per = (nx + 1) * (ny + 1)
+    splits = np.array([0, 10, 20, 30, nz + 1]) * per   # 4 slabs of z-planes
+    parts = [ect.Part(ctx, m, a, splits, r) for r in range(4)]
+    b = m.rhs(w.coil, [w.positions[0]] * 2, [1, 2], w.amplitude)
+    xd, rd = ect.dist_solve(parts, b, tol=1e-8, max_iter=20000)
+    gold = np.load(GOLDEN / "cfg0.npz")
+    fwd_ref = ect.Mesh(ctx, ref_mesh.xyz, ref_mesh.tets, ref_mesh.region).export()["cond_forward"]
+    fwd_new = m.export()["cond_forward"]
+    na = 3 * m.n_nodes
+    back = np.empty(len(xd), np.int64)  # reference dof -> relabelled dof
+    nodes = np.arange(m.n_nodes)
+    for c in range(3):
+        back[3 * nodes + c] = 3 * new_id + c
+    cond = np.flatnonzero(fwd_ref >= 0)
+    back[na + fwd_ref[cond]] = na + fwd_new[new_id[cond]]
+    comp = conductor_components(ref_mesh.tets, ref_mesh.region, fwd_ref)
+    for c in range(2):
+        assert rd[c]["converged"]
+        ea, ev = solution_errors(xd[back, c], gold["x"][c], m.n_nodes, comp)
+        assert ea <= 1e-6 and ev <= 1e-6, (ea, ev)
