@@ -234,6 +234,7 @@ def run_ours(args):
                 "n_dofs": N, "nnz": nnz, "solves_per_position": 4,
                 "rhs_per_matrix_pass": k, "tol": TOL, "solver": "Jacobi-COCG (complex symmetric)",
                 "ms_per_probe_position": elapsed_max / (args.steps * ppb),
+                "probe_positions_per_s": world * args.steps * ppb / (elapsed_max / 1e3),
                 "krylov_iterations_timed": int(iters),
                 "failed_positions": failed_all,
                 "parallelism": f"positions round-robin over {world} GPU(s)",

@@ -155,12 +155,13 @@ def make_cfg1():
 
 
 CFG3_INDEX = 31    # configs[3] position 31 of 64: z = 0.989 cm, the coil pair at the deposit
-CFG3_TOL = 1e-11
+CFG3_TOL = 1e-11   # dZ moves by < 1e-9 relative between solver tolerances 1e-9 and 1e-12
 
 
-def make_cfg3_point():
+def make_cfg3_point(tol=CFG3_TOL, name="cfg3_point.json"):
     """ScanSession::solve_position (scan.cpp:95-143) at one configs[3] position
     on the full configs[1] mesh, through the unmodified reference."""
+    CFG3_TOL = tol
     w = workloads.config3()
     z = w.positions[CFG3_INDEX]
     t0 = time.time()
@@ -188,7 +189,7 @@ def make_cfg3_point():
            "dz": [[v.real, v.imag] for v in dz],
            "modes": [[complex(v).real, complex(v).imag] for v in modes], **info,
            "wall_s": time.time() - t0}
-    (GOLDEN / "cfg3_point.json").write_text(json.dumps(doc, indent=1))
+    (GOLDEN / name).write_text(json.dumps(doc, indent=1))
     print("cfg3 point written", doc, flush=True)
 
 
@@ -295,6 +296,8 @@ if __name__ == "__main__":
         make_cfg0()
     if what in ("cfg3",):
         make_cfg3_point()
+    if what in ("cfg3_1e9",):  # faster variant (same position, looser reference tolerance)
+        make_cfg3_point(1e-9, "cfg3_point.json")
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):
