@@ -17,8 +17,7 @@ check parity against committed data:
                  coil pair next to the deposit): the reference's solve_position
                  chain -- both material configurations assembled (parts = 1),
                  position_rhs for both coils, solve_iterative (GMRES(80)+ILU(0))
-                 at a tight tolerance, delta_impedance x4 and signal_modes.
-                 Hours of single-threaded CPU; run once.
+                 at tol 1e-9, delta_impedance x4 and signal_modes (~10 min).
 
 usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|all]
 """
@@ -155,13 +154,15 @@ def make_cfg1():
 
 
 CFG3_INDEX = 31    # configs[3] position 31 of 64: z = 0.989 cm, the coil pair at the deposit
-CFG3_TOL = 1e-11   # dZ moves by < 1e-9 relative between solver tolerances 1e-9 and 1e-12
+# The reference's GMRES(80)+ILU(0) reaches 1e-9 in ~600 iterations per solve
+# (~4 min each here) but did not reach 1e-11 within 50 min; dZ moves by < 1e-9
+# relative between tolerances 1e-9 and 1e-12 (scripts/cfg3_tol_probe.py on the GPU).
+CFG3_TOL = 1e-9
 
 
 def make_cfg3_point(tol=CFG3_TOL, name="cfg3_point.json"):
     """ScanSession::solve_position (scan.cpp:95-143) at one configs[3] position
     on the full configs[1] mesh, through the unmodified reference."""
-    CFG3_TOL = tol
     w = workloads.config3()
     z = w.positions[CFG3_INDEX]
     t0 = time.time()
@@ -173,10 +174,10 @@ def make_cfg3_point(tol=CFG3_TOL, name="cfg3_point.json"):
     for tag, mats in (("primary", prim), ("reference", refm)):
         s = ref.RefSystem(rm, mats, parts=1, workers=1)
         b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for c in (1, 2)])
-        out = s.solve_iterative_batch(b, tol=CFG3_TOL, max_iter=200000, restart=80, threads=2,
+        out = s.solve_iterative_batch(b, tol=tol, max_iter=200000, restart=80, threads=2,
                                       want_x=True)
         res = [s.relative_residual(out["x"][c], b[c]) for c in range(2)]
-        assert max(res) <= CFG3_TOL * 1.01, res
+        assert max(res) <= tol * 1.01, res
         xs[tag] = out["x"]
         info[tag] = {"iterations": [int(i) for i in out["iterations"]], "true_residual": res,
                      "solve_s": out["seconds"]}
@@ -185,7 +186,7 @@ def make_cfg3_point(tol=CFG3_TOL, name="cfg3_point.json"):
     dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][k], xs["reference"][l])
                    for k in range(2) for l in range(2)])
     modes = ref.signal_modes(dz)
-    doc = {"position_index": CFG3_INDEX, "z": z, "tol": CFG3_TOL, "solver": "GMRES(80)+ILU(0)",
+    doc = {"position_index": CFG3_INDEX, "z": z, "tol": tol, "solver": "GMRES(80)+ILU(0)",
            "dz": [[v.real, v.imag] for v in dz],
            "modes": [[complex(v).real, complex(v).imag] for v in modes], **info,
            "wall_s": time.time() - t0}
@@ -296,8 +297,6 @@ if __name__ == "__main__":
         make_cfg0()
     if what in ("cfg3",):
         make_cfg3_point()
-    if what in ("cfg3_1e9",):  # faster variant (same position, looser reference tolerance)
-        make_cfg3_point(1e-9, "cfg3_point.json")
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):
