@@ -18,8 +18,10 @@ check parity against committed data:
                  chain -- both material configurations assembled (parts = 1),
                  position_rhs for both coils, solve_iterative (GMRES(80)+ILU(0))
                  at tol 1e-9, delta_impedance x4 and signal_modes (~10 min).
+  trace_cfg3.csv the whole configs[3] sweep (64 positions) the same way, in the
+                 reference's trace format (~2 h on 8 cores).
 
-usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|all]
+usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|cfg3_trace|all]
 """
 from __future__ import annotations
 
@@ -194,6 +196,44 @@ def make_cfg3_point(tol=CFG3_TOL, name="cfg3_point.json"):
     print("cfg3 point written", doc, flush=True)
 
 
+def make_cfg3_trace(tol=CFG3_TOL, threads=8):
+    """run_scan (scan.cpp:145-163) over all 64 configs[3] positions on the
+    configs[1] mesh through the unmodified reference: each material
+    configuration assembled once (parts = 1), the 128 coil right-hand sides
+    (position_rhs) solved by solve_iterative (GMRES(80)+ILU(0)) on `threads`
+    host threads, delta_impedance x4 + signal_modes per position, written by
+    the reference's write_trace_csv (scan.cpp:170-207) -> trace_cfg3.csv.
+    About two hours on 8 cores."""
+    w = workloads.config3()
+    zs = np.array(w.positions)
+    t0 = time.time()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    assert two
+    xs, its = {}, {}
+    for tag, mats in (("primary", prim), ("reference", refm)):
+        s = ref.RefSystem(rm, mats, parts=1, workers=1)
+        b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for z in zs for c in (1, 2)])
+        out = s.solve_iterative_batch(b, tol=tol, max_iter=200000, restart=80, threads=threads,
+                                      want_x=True)
+        assert np.all(out["residual"] <= tol * 1.01), out["residual"].max()
+        xs[tag], its[tag] = out["x"], out["iterations"]
+        print(tag, "iterations", int(its[tag].min()), int(its[tag].max()),
+              f"{out['seconds']:.0f}s solve, {time.time() - t0:.0f}s total", flush=True)
+        del s, b
+    dzs, modes = [], []
+    for i in range(len(zs)):
+        dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][2 * i + k],
+                                          xs["reference"][2 * i + l])
+                       for k in range(2) for l in range(2)])
+        dzs.append(dz)
+        modes.append(ref.signal_modes(dz))
+    ref.trace_write(GOLDEN / "trace_cfg3.csv", zs, np.array(dzs), np.array(modes),
+                    config_hash=f"configs[3] GMRES(80)+ILU(0) tol {tol:g}")
+    print("trace_cfg3.csv written", f"{time.time() - t0:.0f}s", flush=True)
+
+
 TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
 
 
@@ -297,6 +337,8 @@ if __name__ == "__main__":
         make_cfg0()
     if what in ("cfg3",):
         make_cfg3_point()
+    if what in ("cfg3_trace",):
+        make_cfg3_trace()
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):
