@@ -55,7 +55,7 @@ def test_gpu_sweep_trace_matches_reference(ctx, tmp_path):
 def test_gpu_configs3_sweep_matches_reference_trace(ctx, tmp_path):
     """BASELINE configs[3] at full size: sweep positions on the configs[1] mesh
     (4 per matrix pass, tol 1e-9) against the reference's own run_scan chain at
-    the same positions (tests/golden/trace_cfg3.csv: 8 of the 64, dense at the
+    the same positions (tests/golden/trace_cfg3.csv: 4 of the 64 around the
     deposit; GMRES(80)+ILU(0) at 1e-9; oracle/make_golden.py cfg3_trace). Bar
     per signal over the curve: max_z |S(z) - S*(z)| / max_z |S*(z)| <= 1e-6
     (SURVEY §8(c) impedance metric); the per-point max_relative_deviation of
