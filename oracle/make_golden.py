@@ -240,6 +240,39 @@ def make_cfg3_trace(tol=CFG3_TOL, threads=8, indices=CFG3_TRACE_INDICES):
     print("trace_cfg3.csv written", f"{time.time() - t0:.0f}s", flush=True)
 
 
+def make_cfg3_trace_seq(indices=(26, 31, 36), tol=CFG3_TOL):
+    """make_cfg3_trace with the positions' two coil solves run one position at
+    a time on 2 threads (the memory-bandwidth-friendly schedule of
+    make_cfg3_point), each matrix assembled once."""
+    w = workloads.config3()
+    zs = np.array([w.positions[i] for i in indices])
+    t0 = time.time()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    xs = {}
+    for tag, mats in (("primary", prim), ("reference", refm)):
+        s = ref.RefSystem(rm, mats, parts=1, workers=1)
+        xs[tag] = []
+        for z in zs:
+            b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for c in (1, 2)])
+            out = s.solve_iterative_batch(b, tol=tol, max_iter=5000, restart=80, threads=2,
+                                          want_x=True)
+            assert np.all(out["residual"] <= tol * 1.01), out["residual"]
+            xs[tag].append(out["x"])
+            print(tag, f"z={z:.6g}", list(out["iterations"]), f"{time.time() - t0:.0f}s", flush=True)
+        del s
+    dzs, modes = [], []
+    for i in range(len(zs)):
+        dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][i][k], xs["reference"][i][l])
+                       for k in range(2) for l in range(2)])
+        dzs.append(dz)
+        modes.append(ref.signal_modes(dz))
+    ref.trace_write(GOLDEN / "trace_cfg3.csv", zs, np.array(dzs), np.array(modes),
+                    config_hash=f"configs[3] GMRES(80)+ILU(0) tol {tol:g}")
+    print("trace_cfg3.csv written", f"{time.time() - t0:.0f}s", flush=True)
+
+
 TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
 
 
