@@ -63,23 +63,31 @@ typedef struct ect_materials {
   double z_surface[2];       /* surface impedance (re, im) used when ibc_enabled */
 } ect_materials;
 
-/* RunConfig [materials] keys (config.hpp:25-39). Negative sigma_defect /
- * mu_r_defect mean "unset" (defaults to the tube values, config.cpp:333-334). */
+/* RunConfig [materials] keys (config.hpp:25-39), same defaults. Fill with
+ * ect_physics_init() and override fields; the values are validated as
+ * RunConfig's parser does (config.cpp:218-236: positive frequency, sigmas,
+ * mu_r, sigma_eps_ratio, bc_penalty, 0 < delta_gauge < 1) -> ECT_ERR_CONFIG.
+ * sigma_defect / mu_r_defect are std::optional in the reference: NaN means
+ * unset (defaults to the tube values, config.cpp:334-335). */
 typedef struct ect_physics {
-  double frequency;
-  double sigma_tube;
-  double mu_r_tube;
-  double sigma_defect;
-  double mu_r_defect;
-  double sigma_eps_ratio;
-  double delta_gauge;
-  double bc_penalty;
-  int32_t mu_tilde_harmonic;
-  double mu_tilde_fixed;
-  double sigma_tsp;  /* < 0: default 5e6 (config.hpp:29) */
-  double mu_r_tsp;   /* < 0: default 50 (config.hpp:30) */
-  int32_t ibc_tsp;   /* materials.ibc_tsp (config.hpp:38): plate as surface impedance */
+  double frequency;        /* 100e3 */
+  double sigma_tube;       /* 1e6 */
+  double mu_r_tube;        /* 1 */
+  double sigma_defect;     /* NaN = unset */
+  double mu_r_defect;      /* NaN = unset */
+  double sigma_eps_ratio;  /* 1e-6 */
+  double delta_gauge;      /* 1e-6 */
+  double bc_penalty;       /* 1e13 */
+  int32_t mu_tilde_harmonic; /* 1: mu_tilde_policy = harmonic, 0: fixed */
+  double mu_tilde_fixed;   /* kMu0 */
+  double sigma_tsp;        /* 5e6 (config.hpp:29) */
+  double mu_r_tsp;         /* 50 (config.hpp:30) */
+  int32_t ibc_tsp;         /* materials.ibc_tsp (config.hpp:38): plate as surface impedance */
+  int32_t l22_sigma_eps;   /* materials.l22_sigma_eps (config.hpp:39) */
 } ect_physics;
+
+/* RunConfig's [materials] defaults (config.hpp:25-39). */
+void ect_physics_init(ect_physics* physics);
 
 /* CoilPair (tube_mesh.hpp:13-21). */
 typedef struct ect_coil {
@@ -131,6 +139,8 @@ typedef struct ect_timings {
   int64_t vec_launches;
   int64_t spmv_partial_launches;
   int64_t vec_partial_launches;
+  double precond_ms_total;  /* multigrid cycles inside the solve (sampled as the SpMV) */
+  int64_t precond_launches;
 } ect_timings;
 
 /* ---- context --------------------------------------------------------- */
@@ -149,10 +159,9 @@ int ect_ctx_synchronize(ect_ctx* ctx);
  * storage comparison). */
 #define ECT_FORMAT_NB 0
 #define ECT_FORMAT_CSR 1
-#define ECT_FORMAT_NB_TILED 2 /* NB + shared-memory x tiles (measured slower on B200) */
 #define ECT_FORMAT_SELL 3     /* SELL-32-sigma (sigma = 256), configs[2]'s comparison */
 int ect_ctx_set_format(ect_ctx* ctx, int format);
-/* 0: CSR, 1: NB untiled, 2: NB with shared-memory x tiles, 3: SELL-C-sigma. */
+/* 0: CSR, 1: NB (sliced-ELL node blocks), 3: SELL-C-sigma. */
 int ect_matrix_format(ect_matrix* m, int32_t* nb);
 /* NB storage counts: 3x3 node blocks and conductor couplings (0 for CSR). */
 int ect_matrix_nb_counts(ect_matrix* m, int64_t* blocks, int64_t* couplings);
@@ -209,9 +218,21 @@ int ect_harmonic_mu_tilde(ect_mesh* mesh, const ect_materials* mats, double* out
  * structurally symmetric, so the CSR row_ptr/col_idx returned here are
  * bit-identical to the reference's col_ptr/row_idx. */
 int ect_matrix_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix** out);
-/* Upload an external CSR (e.g. the oracle's) for SpMV/solve parity. */
+/* The reference's own matrix type as the input: CscMatrix {n_rows = n_cols = n,
+ * col_ptr[n+1], row_idx[nnz], values[nnz]} (sparse.hpp:56-66) exactly as
+ * build_global / from_triplets produce it, e.g. a GlobalSystem::matrix handed
+ * to solve_iterative (solver.hpp:69-70). Transposed on the device into the
+ * CSR the kernels stream (no assumption that the pattern is symmetric). A
+ * value-symmetry probe (max |a_ij - a_ji| <= 1e-12 sqrt(|a_ii a_jj|) over the
+ * stored pattern) decides the Krylov method: COCG for A = A^T, BiCGStab
+ * otherwise (impedance surface terms make A non-symmetric). */
+int ect_matrix_from_csc(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* col_ptr,
+                        const int32_t* row_idx, const double* values, ect_matrix** out);
+/* Same for an external CSR (row_ptr, col_idx, values). */
 int ect_matrix_from_csr(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* row_ptr,
                         const int32_t* col_idx, const double* values, ect_matrix** out);
+/* 1 if the matrix is complex symmetric (COCG), 0 if not (BiCGStab). */
+int ect_matrix_symmetric(ect_matrix* m, int32_t* symmetric);
 int ect_matrix_destroy(ect_matrix* m);
 int ect_matrix_counts(ect_matrix* m, int64_t* n, int64_t* nnz);
 /* K2: assemble_system + apply_essential_bc + build_global values
@@ -227,18 +248,44 @@ int ect_matrix_export_csc(ect_matrix* m, int32_t* col_ptr, int32_t* row_idx, dou
 
 /* ---- right-hand sides ----------------------------------------------------
  * K3: coil_support + assemble_rhs + apply_pins_to_rhs for n_rhs (probe z,
- * coil) pairs (tube_mesh.cpp:272-288, assembly.cpp:329-378, scan.cpp:87-93).
- * Output column r of an interleaved [n_dofs][n_rhs] complex array. */
+ * coil) pairs (tube_mesh.cpp:272-288, assembly.cpp:329-378, scan.cpp:87-93 =
+ * ScanSession::position_rhs). Output column r of an interleaved
+ * [n_dofs][n_rhs] complex array. */
 int ect_rhs_coil(ect_ctx* ctx, ect_mesh* mesh, const ect_coil* coil, const double* probe_z,
                  const int32_t* which_coil, int32_t n_rhs, double amplitude, double* rhs);
+/* assemble_rhs(mesh, support_tets, amplitude, total_dofs) (assembly.hpp:84-85,
+ * assembly.cpp:335-378): caller-supplied support tets (any order, duplicates
+ * allowed); NOT pinned, as the reference (use ect_apply_pins_to_rhs).
+ * Errors as the reference: empty support, support in a conductor (ECT_ERR_MESH). */
+int ect_rhs_support(ect_ctx* ctx, ect_mesh* mesh, const int32_t* support_tets,
+                    int64_t n_support, double amplitude, double* rhs);
+/* assemble_rhs(mesh, coil_tag, amplitude, total_dofs) (assembly.hpp:86-87,
+ * assembly.cpp:380-384): the support is every tet of region coil_tag. */
+int ect_rhs_region(ect_ctx* ctx, ect_mesh* mesh, int32_t coil_tag, double amplitude, double* rhs);
+/* apply_pins_to_rhs (assembly.hpp:79, assembly.cpp:329-333) on n_rhs
+ * interleaved vectors: every pinned A-dof entry = bc_penalty * 0. */
+int ect_apply_pins_to_rhs(ect_ctx* ctx, ect_mesh* mesh, double* rhs, int32_t n_rhs);
 
 /* ---- SpMV / solve --------------------------------------------------------
  * K4: y = A x (CscMatrix::multiply, sparse.cpp:115-124) for n_rhs vectors in
  * interleaved [n][n_rhs] layout. */
 int ect_spmv(ect_ctx* ctx, ect_matrix* m, const double* x, double* y, int32_t n_rhs);
-/* K5/K6: solve_iterative (iterative.cpp:109-228) replacement: Jacobi-
- * preconditioned COCG (A is complex symmetric) for n_rhs right-hand sides
- * sharing one matrix pass per iteration; true-residual confirmation as
+/* Preconditioner of the Krylov solve. ECT_PRECOND_JACOBI: point Jacobi.
+ * ECT_PRECOND_AMG (default): one aggregation-multigrid W-cycle per iteration
+ * (greedy node aggregation, Galerkin coarse operators with the plain transpose
+ * so the preconditioner stays complex symmetric for COCG, damped-Jacobi
+ * smoothing, dense coarsest solve) — the GPU replacement for the reference's
+ * ILU(0) (iterative.cpp:59-105), built once per matrix. The context default
+ * applies to matrices created afterwards (sessions included). */
+#define ECT_PRECOND_JACOBI 0
+#define ECT_PRECOND_AMG 1
+int ect_ctx_set_preconditioner(ect_ctx* ctx, int32_t precond);
+int ect_matrix_set_preconditioner(ect_matrix* m, int32_t precond);
+/* info: levels, setup ms, operator complexity (sum nnz / fine nnz), coarsest n */
+int ect_matrix_precond_info(ect_matrix* m, double info[4]);
+/* K5/K6: solve_iterative (iterative.cpp:109-228) replacement: preconditioned
+ * COCG (A complex symmetric; BiCGStab when it is not) for n_rhs right-hand
+ * sides sharing one matrix pass per iteration; true-residual confirmation as
  * iterative.cpp:208-216. b, x interleaved [n][n_rhs]. Non-convergence is
  * reported in results (not an error), breakdown returns ECT_ERR_SOLVER. */
 int ect_solve(ect_ctx* ctx, ect_matrix* m, const double* b, double* x, int32_t n_rhs,

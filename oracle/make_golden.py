@@ -18,8 +18,10 @@ check parity against committed data:
                  chain -- both material configurations assembled (parts = 1),
                  position_rhs for both coils, solve_iterative (GMRES(80)+ILU(0))
                  at tol 1e-9, delta_impedance x4 and signal_modes (~10 min).
-  trace_cfg3.csv 4 configs[3] positions around the deposit the same way, in the
-                 reference's trace format.
+  trace_cfg3.csv 8 configs[3] positions (both ends, both deposit edges, the
+                 centre, 3 fill) the same way at GMRES tol 1e-10, in the
+                 reference's trace format; trace_cfg3.json = per-position
+                 checkpoint (iterations, true residuals, solve seconds).
 
 usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|cfg3_trace|all]
 """
@@ -196,81 +198,81 @@ def make_cfg3_point(tol=CFG3_TOL, name="cfg3_point.json"):
     print("cfg3 point written", doc, flush=True)
 
 
-# configs[3] positions of the reference trace: 4 of the 64 around the deposit
-# (z in [0.9, 1.1] cm = positions 26-36): one right-hand side per host thread.
-# Eight GMRES(80)+ILU(0) solves share this container's memory bandwidth, ~5x
-# slower each than alone; all 64 positions would take most of a day here.
-CFG3_TRACE_INDICES = (20, 26, 31, 36)
+# Round-2 configs[3] golden: both far-field ends, both deposit edges (z = 0.9 /
+# 1.1 cm are positions 26 / 36), the centre (31) and three fill positions; run
+# in this order so that an interrupted run still holds the important ones.
+CFG3_TRACE8_INDICES = (31, 26, 36, 0, 63, 20, 45, 13)
+CFG3_TRACE8_TOL = 1e-10
+CFG3_TRACE8_RESTART = 120
 
 
-def make_cfg3_trace(tol=CFG3_TOL, threads=8, indices=CFG3_TRACE_INDICES):
-    """run_scan (scan.cpp:145-163) over configs[3] positions on the configs[1]
-    mesh through the unmodified reference: each material configuration
-    assembled once (parts = 1), the coil right-hand sides (position_rhs) solved
-    by solve_iterative (GMRES(80)+ILU(0)) on `threads` host threads,
-    delta_impedance x4 + signal_modes per position, written by the reference's
-    write_trace_csv (scan.cpp:170-207) -> trace_cfg3.csv."""
+def make_cfg3_trace8(indices=CFG3_TRACE8_INDICES, tol=CFG3_TRACE8_TOL,
+                     restart=CFG3_TRACE8_RESTART, threads=4,
+                     ckpt=GOLDEN / "trace_cfg3.json"):
+    """run_scan (scan.cpp:145-163) restricted to `indices` of the 64 configs[3]
+    positions, through the unmodified reference: both material configurations
+    assembled once (parts = 1) and kept resident, then per position the four
+    solve_position solves (2 coils x 2 configurations, scan.cpp:103-135) run
+    concurrently by solve_iterative (GMRES(restart)+ILU(0), iterative.cpp:
+    109-228), each accepted only when its TRUE residual (relative_residual,
+    sparse.cpp:135-145) is <= tol, then delta_impedance x4 + signal_modes.
+    After every position the JSON checkpoint and trace_cfg3.csv (the
+    reference's write_trace_csv, scan.cpp:170-207, sorted by z) are rewritten,
+    so an interrupted run keeps every finished position."""
+    import threading
+
     w = workloads.config3()
-    zs = np.array([w.positions[i] for i in indices])
     t0 = time.time()
     mesh = w.mesh()
     rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
     prim, refm, two = rm.materials(w.physics)
-    assert two
-    xs, its = {}, {}
-    for tag, mats in (("primary", prim), ("reference", refm)):
-        s = ref.RefSystem(rm, mats, parts=1, workers=1)
-        b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for z in zs for c in (1, 2)])
-        out = s.solve_iterative_batch(b, tol=tol, max_iter=5000, restart=80, threads=threads,
-                                      want_x=True)
-        assert np.all(out["residual"] <= tol * 1.01), out["residual"].max()
-        xs[tag], its[tag] = out["x"], out["iterations"]
-        print(tag, "iterations", int(its[tag].min()), int(its[tag].max()),
-              f"{out['seconds']:.0f}s solve, {time.time() - t0:.0f}s total", flush=True)
-        del s, b
-    dzs, modes = [], []
-    for i in range(len(zs)):
-        dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][2 * i + k],
-                                          xs["reference"][2 * i + l])
-                       for k in range(2) for l in range(2)])
-        dzs.append(dz)
-        modes.append(ref.signal_modes(dz))
-    ref.trace_write(GOLDEN / "trace_cfg3.csv", zs, np.array(dzs), np.array(modes),
-                    config_hash=f"configs[3] GMRES(80)+ILU(0) tol {tol:g}")
-    print("trace_cfg3.csv written", f"{time.time() - t0:.0f}s", flush=True)
+    assert two, "configs[3] has a deposit: two material configurations"
+    done = json.loads(ckpt.read_text()) if ckpt.exists() else {"points": {}}
+    done.update(tol=tol, solver=f"GMRES({restart})+ILU(0)", mesh="configs[1]")
+    systems = {tag: ref.RefSystem(rm, mats, parts=1, workers=1)
+               for tag, mats in (("primary", prim), ("reference", refm))}
+    print(f"assembled both configurations {time.time() - t0:.0f}s", flush=True)
+    per = max(1, threads // 2)
+    for i in indices:
+        if str(i) in done["points"]:
+            continue
+        z = w.positions[i]
+        out = {}
 
-
-def make_cfg3_trace_seq(indices=(26, 31, 36), tol=CFG3_TOL):
-    """make_cfg3_trace with the positions' two coil solves run one position at
-    a time on 2 threads (the memory-bandwidth-friendly schedule of
-    make_cfg3_point), each matrix assembled once."""
-    w = workloads.config3()
-    zs = np.array([w.positions[i] for i in indices])
-    t0 = time.time()
-    mesh = w.mesh()
-    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
-    prim, refm, two = rm.materials(w.physics)
-    xs = {}
-    for tag, mats in (("primary", prim), ("reference", refm)):
-        s = ref.RefSystem(rm, mats, parts=1, workers=1)
-        xs[tag] = []
-        for z in zs:
+        def run(tag):
+            s = systems[tag]
             b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for c in (1, 2)])
-            out = s.solve_iterative_batch(b, tol=tol, max_iter=5000, restart=80, threads=2,
-                                          want_x=True)
-            assert np.all(out["residual"] <= tol * 1.01), out["residual"]
-            xs[tag].append(out["x"])
-            print(tag, f"z={z:.6g}", list(out["iterations"]), f"{time.time() - t0:.0f}s", flush=True)
-        del s
-    dzs, modes = [], []
-    for i in range(len(zs)):
-        dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][i][k], xs["reference"][i][l])
+            r = s.solve_iterative_batch(b, tol=tol, max_iter=20000, restart=restart,
+                                        threads=per, want_x=True)
+            r["true"] = [s.relative_residual(r["x"][c], b[c]) for c in range(2)]
+            out[tag] = r
+
+        ts = [threading.Thread(target=run, args=(tag,)) for tag in systems]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        true = out["primary"]["true"] + out["reference"]["true"]
+        assert max(true) <= tol * 1.01, (i, true)
+        dz = np.array([rm.delta_impedance(prim, refm, out["primary"]["x"][k],
+                                          out["reference"]["x"][l])
                        for k in range(2) for l in range(2)])
-        dzs.append(dz)
-        modes.append(ref.signal_modes(dz))
-    ref.trace_write(GOLDEN / "trace_cfg3.csv", zs, np.array(dzs), np.array(modes),
-                    config_hash=f"configs[3] GMRES(80)+ILU(0) tol {tol:g}")
-    print("trace_cfg3.csv written", f"{time.time() - t0:.0f}s", flush=True)
+        modes = ref.signal_modes(dz)
+        done["points"][str(i)] = {
+            "z": z, "dz": [[v.real, v.imag] for v in dz],
+            "modes": [[complex(v).real, complex(v).imag] for v in modes],
+            "iterations": [int(v) for tag in systems for v in out[tag]["iterations"]],
+            "true_residual": true,
+            "solve_s": max(out[tag]["seconds"] for tag in systems)}
+        ckpt.write_text(json.dumps(done, indent=1))
+        pts = sorted(done["points"].values(), key=lambda p: p["z"])
+        ref.trace_write(GOLDEN / "trace_cfg3.csv", [p["z"] for p in pts],
+                        [[complex(*v) for v in p["dz"]] for p in pts],
+                        [[complex(*v) for v in p["modes"]] for p in pts],
+                        config_hash=f"configs[3] GMRES({restart})+ILU(0) tol {tol:g}")
+        print(f"position {i} z={z:.6g} its={done['points'][str(i)]['iterations']} "
+              f"res={max(true):.2e} {time.time() - t0:.0f}s", flush=True)
+    print("trace_cfg3.csv complete", f"{time.time() - t0:.0f}s", flush=True)
 
 
 TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
@@ -377,7 +379,7 @@ if __name__ == "__main__":
     if what in ("cfg3",):
         make_cfg3_point()
     if what in ("cfg3_trace",):
-        make_cfg3_trace()
+        make_cfg3_trace8()
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):

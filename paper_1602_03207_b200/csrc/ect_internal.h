@@ -92,6 +92,30 @@ struct Profile {
   int64_t launches = 0;
 };
 
+// Aggregation multigrid hierarchy (amg.cu setup, krylov.cu cycle). Level 0
+// is the matrix itself; level l+1 = P_l^T A_l P_l with the plain-aggregation
+// prolongator P_l (0/1 entries: dof i -> coarse dof cmap[i], -1 for
+// Dirichlet-pinned dofs), coarsest level inverted densely.
+struct AmgLevel {
+  int64_t n = 0, nnz = 0;
+  DevBuf<int> row_ptr, col;          // levels >= 1 (level 0 streams the ect_matrix)
+  DevBuf<double2> val, dinv;
+  int64_t n_next = 0;
+  DevBuf<int> cmap;                  // [n] coarse dof of each dof (-1: not aggregated)
+  DevBuf<int> r_ptr, r_idx;          // coarse dof -> its dofs, ascending
+  DevBuf<double2> xt, t, b, out, b2, out2;  // cycle work vectors [n][kcap]
+};
+struct Amg {
+  std::vector<AmgLevel> lv;          // lv.back() is the dense coarsest level
+  DevBuf<double2> minv;              // [n][n] row-major inverse of the coarsest matrix
+  double omega = 0.6;                // damped-Jacobi weight
+  double oc = 1.5;                   // coarse-correction over-weighting
+  int wcycle = 1;                    // 1: W-cycle (two coarse visits per level), 0: V
+  int kcap = 0;                      // batch width the work vectors hold
+  double setup_ms = 0.0;
+  double op_complexity = 0.0;        // sum of level nnz / fine nnz
+};
+
 }  // namespace ect
 
 struct ect_ctx {
@@ -103,8 +127,9 @@ struct ect_ctx {
   ect_timings timings{};
   ect::Profile prof;
   // pinned staging for host<->device copies
-  void* pinned = nullptr;
+  void* pinned = nullptr;                      // two staging halves (ectgpu.cpp copy_h2d/d2h)
   size_t pinned_bytes = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   int* pinned_flag = nullptr;  // small pinned word for convergence polling
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
@@ -112,18 +137,16 @@ struct ect_ctx {
   cudaEvent_t ev_h1 = nullptr, ev_h2 = nullptr;
   bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
   bool use_sell = false;                        // ect_ctx_set_format(ctx, ECT_FORMAT_SELL)
-  bool use_nbe = true;                          // NB-E sliced-ELL blocks (default; variants 1..49 off)
+  int precond = ECT_PRECOND_AMG;                // default for matrices created afterwards
   int sell_sigma = 256;
   struct SolverWorkspace {                      // cocg_solve buffers, reused across solves
-    ect::DevBuf<double2> bb, xx, r, p, q;
+    ect::DevBuf<double2> bb, xx, r, p, q, z;
     ect::DevBuf<double2> rh, ph, sh, t;         // BiCGStab extras
     ect::DevBuf<ect::RhsState> st;
     ect::DevBuf<int> n_active;
     ect::DevBuf<unsigned> counter;
     ect::DevBuf<double> partial;
   } ws;
-  bool no_tiles = true;                         // NB-T only with ect_ctx_set_format(ECT_FORMAT_NB_TILED)
-  int nb_variant = 0;                           // NB SpMV kernel variant (ECT_NB_VARIANT)
 };
 
 struct ect_mesh {
@@ -159,8 +182,14 @@ struct ect_mesh {
   ect::DevBuf<int> ibc_inc;
 };
 
+#include <memory>
+
 struct ect_matrix {
   ect_ctx* ctx = nullptr;
+  ect_mesh* mesh = nullptr;         // the mesh a from-mesh pattern was built on (borrowed)
+  int precond = ECT_PRECOND_JACOBI;  // ECT_PRECOND_* used by ect_solve / the session
+  std::unique_ptr<ect::Amg> amg;    // built on first use of ECT_PRECOND_AMG
+  int64_t n_zero_diag = 0;          // Jacobi: rows without a usable diagonal
   int64_t n = 0, nnz = 0;
   int64_t n_nodes = 0, n_cond = 0;  // DOF structure when built from a mesh
   bool from_mesh = false;
@@ -175,7 +204,6 @@ struct ect_matrix {
   // 6 double2 planes) over the neighbour list, and conductor couplings
   // (A-V column, V-A row, V-V entry: 4 double2 planes).
   bool has_nb = false;
-  int nbs_cap[3] = {-1, -1, -1};    // staged SpMV ring-slot blocks for 4 / 8 / 16 nodes per warp
   int64_t nb_blocks = 0, nb_ncpl = 0;
   const int* nb_blk_ptr = nullptr;  // = mesh->nbr_off (borrowed)
   const int* nb_blk_col = nullptr;  // = mesh->nbr (borrowed)
@@ -194,12 +222,6 @@ struct ect_matrix {
   int64_t sell_chunks = 0, sell_stored = 0;
   ect::DevBuf<int> sell_off, sell_perm, sell_col;
   ect::DevBuf<double2> sell_val;
-  // NB-T: tiles of consecutive nodes with a staged x footprint
-  bool has_nbt = false;
-  int64_t nbt_tiles = 0;
-  int nbt_fmax = 0;
-  ect::DevBuf<int> nbt_fp_off, nbt_fp_node;
-  ect::DevBuf<uint16_t> nbt_lcol, nbt_cpl_lcol;
 };
 
 #include "dist_plan.h"
@@ -241,6 +263,9 @@ bool is_device_ptr(const void* p);
 void build_mesh_topology(ect_mesh* m);                         // mesh.cu
 void build_pattern(ect_mesh* m, ect_matrix* a);                // pattern.cu
 void export_csc_values(ect_matrix* a, double2* out);           // pattern.cu (symmetric pattern)
+// External CSC (csc = true) or CSR arrays on the device -> a's CSR + symmetry probe
+void matrix_from_compressed(ect_ctx* ctx, int64_t n, int64_t nnz, const int* ptr, const int* idx,
+                            const double2* val, bool csc, ect_matrix* a);  // pattern.cu
 void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a);  // assembly.cu
 void compute_jacobi(ect_matrix* a);                            // krylov.cu
 void build_nb(ect_mesh* m, ect_matrix* a);                     // krylov.cu (NB format)
@@ -248,6 +273,9 @@ void build_sell(ect_matrix* a, int sigma);                     // krylov.cu (SEL
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k);  // spmv.cu
 void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* which, int n_rhs,
                double amplitude, double2* rhs);                // rhs.cu
+void build_rhs_support(ect_mesh* m, const int* support, int64_t n_support, int region_tag,
+                       double amplitude, double2* rhs);  // rhs.cu (support == nullptr: region)
+void apply_pins_rhs(ect_mesh* m, double2* rhs, int n_rhs);  // rhs.cu
 void delta_impedance(ect_mesh* m, const ect_materials& p, const ect_materials& r,
                      const double2* xk1, const double2* xk2, const double2* xl1,
                      const double2* xl2, int stride, double2 out[4]);  // signals.cu
@@ -255,9 +283,13 @@ struct SolveOut {
   std::vector<int> iters;
   std::vector<double> residual;
   std::vector<int> converged;
+  std::vector<int> breakdown;  // per column: the Krylov recurrence broke down
 };
+// ect_solve's contract (iterative.cpp:176): a breakdown is a SolverError
+void throw_on_breakdown(const SolveOut& out);
 void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
                 const ect_iter_options& opt, SolveOut* out);  // krylov.cu
+void amg_setup(ect_matrix* a);                                  // amg.cu
 
 // distributed solve (krylov.cu)
 ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_parts, int part);

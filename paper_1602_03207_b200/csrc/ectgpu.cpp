@@ -42,6 +42,81 @@ void require(bool ok, int code, const char* what) {
   if (!ok) ect::fail(code, what);
 }
 
+// Host <-> device copies of caller buffers. Page-locked host memory (the
+// caller's cudaHostAlloc / cudaHostRegister / torch pin_memory) is copied
+// directly and asynchronously; pageable memory goes through the context's
+// two pinned staging halves (kStageHalf bytes each, allocated once), the
+// memcpy into one half overlapping the DMA out of the other.
+constexpr size_t kStageHalf = 16u << 20;
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
+char* stage_buffer(ect_ctx* ctx) {
+  if (!ctx->pinned) {
+    CK(cudaHostAlloc(&ctx->pinned, 2 * kStageHalf, cudaHostAllocDefault));
+    ctx->pinned_bytes = 2 * kStageHalf;
+    CK(cudaEventCreateWithFlags(&ctx->stage_ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->stage_ev[1], cudaEventDisableTiming));
+  }
+  return static_cast<char*>(ctx->pinned);
+}
+
+void copy_h2d(ect_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  if (is_pinned_host(src)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return;
+  }
+  char* st = stage_buffer(ctx);
+  bool used[2] = {false, false};
+  for (size_t off = 0, q = 0; off < bytes; off += kStageHalf, ++q) {
+    const int h = (int)(q & 1);
+    const size_t len = std::min(kStageHalf, bytes - off);
+    if (used[h]) CK(cudaEventSynchronize(ctx->stage_ev[h]));  // DMA out of this half done
+    std::memcpy(st + h * kStageHalf, static_cast<const char*>(src) + off, len);
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, st + h * kStageHalf, len,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->stage_ev[h], ctx->stream));
+    used[h] = true;
+  }
+  // the staging halves are reused by the next call: wait for the last DMAs
+  for (int h = 0; h < 2; ++h)
+    if (used[h]) CK(cudaEventSynchronize(ctx->stage_ev[h]));
+}
+
+void copy_d2h(ect_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  if (is_pinned_host(dst)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  char* st = stage_buffer(ctx);
+  const size_t n_chunks = (bytes + kStageHalf - 1) / kStageHalf;
+  auto issue = [&](size_t q) {
+    const size_t off = q * kStageHalf, len = std::min(kStageHalf, bytes - off);
+    const int h = (int)(q & 1);
+    CK(cudaMemcpyAsync(st + h * kStageHalf, static_cast<const char*>(src) + off, len,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(ctx->stage_ev[h], ctx->stream));
+  };
+  issue(0);
+  for (size_t q = 0; q < n_chunks; ++q) {
+    const int h = (int)(q & 1);
+    CK(cudaEventSynchronize(ctx->stage_ev[h]));
+    if (q + 1 < n_chunks) issue(q + 1);  // next DMA into the other half overlaps this memcpy
+    const size_t off = q * kStageHalf, len = std::min(kStageHalf, bytes - off);
+    std::memcpy(static_cast<char*>(dst) + off, st + h * kStageHalf, len);
+  }
+}
+
 // Input buffer that may live on the host or on the context's device.
 template <typename T>
 struct In {
@@ -53,7 +128,7 @@ struct In {
       return;
     }
     tmp.alloc(count);
-    CK(cudaMemcpyAsync(tmp.p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    copy_h2d(ctx, tmp.p, p, count * sizeof(T));
     dev = tmp.p;
   }
 };
@@ -76,8 +151,16 @@ struct Out {
     dev = tmp.p;
   }
   void finish() {
-    if (host) CK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    if (host) copy_d2h(ctx, host, dev, count * sizeof(T));
     CK(cudaStreamSynchronize(ctx->stream));
+  }
+};
+
+// In-place buffer (read and written).
+template <typename T>
+struct InOut : Out<T> {
+  InOut(ect_ctx* c, T* p, size_t n) : Out<T>(c, p, n) {
+    if (this->host) copy_h2d(c, this->dev, p, n * sizeof(T));
   }
 };
 
@@ -195,10 +278,6 @@ int ect_ctx_create(int device, ect_ctx** out) {
                                   prop.name);
     }
     ctx->num_sms = prop.multiProcessorCount;
-    if (const char* v = std::getenv("ECT_NB_VARIANT")) ctx->nb_variant = std::atoi(v);
-    // NB-E (sliced-ELL blocks) is the default SpMV layout; variants 1..49 select
-    // the per-node NB kernels it was measured against
-    ctx->use_nbe = ctx->nb_variant == 0 || ctx->nb_variant >= 50;
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&ctx->ev_a));
     CK(cudaEventCreate(&ctx->ev_b));
@@ -215,6 +294,9 @@ int ect_ctx_destroy(ect_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (auto e : ctx->stage_ev)
+      if (e) cudaEventDestroy(e);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
     for (auto e : ctx->marks) cudaEventDestroy(e);
@@ -244,18 +326,16 @@ int ect_ctx_set_profiling(ect_ctx* ctx, int enabled) {
 
 int ect_ctx_set_format(ect_ctx* ctx, int format) {
   return guarded([&] {
-    require(format == ECT_FORMAT_NB || format == ECT_FORMAT_CSR ||
-                format == ECT_FORMAT_NB_TILED || format == ECT_FORMAT_SELL,
+    require(format == ECT_FORMAT_NB || format == ECT_FORMAT_CSR || format == ECT_FORMAT_SELL,
             ECT_ERR_CONFIG, "ect_ctx_set_format: unknown format");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ctx->force_csr = format == ECT_FORMAT_CSR || format == ECT_FORMAT_SELL;
     ctx->use_sell = format == ECT_FORMAT_SELL;
-    ctx->no_tiles = format != ECT_FORMAT_NB_TILED;
   });
 }
 
 int ect_matrix_format(ect_matrix* m, int32_t* nb) {
-  return guarded([&] { *nb = m->has_nb ? (m->has_nbt ? 2 : 1) : (m->has_sell ? 3 : 0); });
+  return guarded([&] { *nb = m->has_nb ? 1 : (m->has_sell ? 3 : 0); });
 }
 
 int ect_matrix_nb_counts(ect_matrix* m, int64_t* blocks, int64_t* couplings) {
@@ -410,38 +490,71 @@ int ect_harmonic_mu_tilde(ect_mesh* m, const ect_materials* mats, double* out) {
   });
 }
 
+void ect_physics_init(ect_physics* ph) {
+  // RunConfig's [materials] defaults (config.hpp:25-39)
+  if (!ph) return;
+  *ph = ect_physics{};
+  ph->frequency = 100e3;
+  ph->sigma_tube = 1e6;
+  ph->mu_r_tube = 1.0;
+  ph->sigma_defect = std::nan("");  // std::optional: unset
+  ph->mu_r_defect = std::nan("");
+  ph->sigma_eps_ratio = 1e-6;
+  ph->delta_gauge = 1e-6;
+  ph->bc_penalty = 1e13;
+  ph->mu_tilde_harmonic = 1;
+  ph->mu_tilde_fixed = kMu0;
+  ph->sigma_tsp = 5e6;
+  ph->mu_r_tsp = 50.0;
+  ph->ibc_tsp = 0;
+  ph->l22_sigma_eps = 0;
+}
+
 int ect_materials_from_physics(ect_mesh* mesh, const ect_physics* ph, ect_materials* primary,
                                ect_materials* reference, int32_t* two_configs) {
   return guarded([&] {
-    // RunConfig::material_table (config.cpp:325-347); TSP keeps its defaults
-    // (config.hpp:29-30), IBC off.
-    require(ph->frequency > 0 && ph->sigma_tube >= 0, ECT_ERR_CONFIG, "physics: bad frequency/sigma");
+    require(ph != nullptr, ECT_ERR_CONFIG, "physics: null");
+    // RunConfig validation (config.cpp:218-236)
+    auto need = [](bool ok, const char* key, const char* what) {
+      if (!ok) ect::fail(ECT_ERR_CONFIG, std::string(key) + ": " + what);
+    };
+    need(ph->frequency > 0.0, "materials.frequency", "must be positive");
+    need(ph->sigma_tube > 0.0, "materials.sigma_tube", "must be positive");
+    need(ph->mu_r_tube > 0.0, "materials.mu_r_tube", "must be positive");
+    need(ph->sigma_tsp > 0.0, "materials.sigma_tsp", "must be positive");
+    need(ph->mu_r_tsp > 0.0, "materials.mu_r_tsp", "must be positive");
+    const bool has_sd = !std::isnan(ph->sigma_defect), has_md = !std::isnan(ph->mu_r_defect);
+    if (has_sd) need(ph->sigma_defect > 0.0, "materials.sigma_defect", "must be positive");
+    if (has_md) need(ph->mu_r_defect > 0.0, "materials.mu_r_defect", "must be positive");
+    need(ph->sigma_eps_ratio > 0.0, "materials.sigma_eps_ratio", "must be positive");
+    need(ph->delta_gauge > 0.0 && ph->delta_gauge < 1.0, "materials.delta_gauge",
+         "must lie in (0, 1)");
+    need(ph->bc_penalty > 0.0, "materials.bc_penalty", "must be positive");
+    if (!ph->mu_tilde_harmonic) need(ph->mu_tilde_fixed > 0.0, "materials.mu_tilde", "must be positive");
+    // RunConfig::material_table (config.cpp:325-347)
     ect_materials m{};
     m.omega = 2.0 * std::numbers::pi * ph->frequency;
     m.sigma_eps = ph->sigma_eps_ratio * ph->sigma_tube;
     m.delta_gauge = ph->delta_gauge;
     m.bc_penalty = ph->bc_penalty;
-    m.l22_use_sigma_eps = 0;
+    m.l22_use_sigma_eps = ph->l22_sigma_eps ? 1 : 0;
     m.ibc_enabled = 0;
     auto set = [&m](int r, double s, double mu) {
       m.sigma[r] = s;
       m.mu[r] = mu;
     };
     set(ECT_REGION_TUBE, ph->sigma_tube, kMu0 * ph->mu_r_tube);
-    set(ECT_REGION_TSP, ph->sigma_tsp >= 0 ? ph->sigma_tsp : 5e6,
-        kMu0 * (ph->mu_r_tsp >= 0 ? ph->mu_r_tsp : 50.0));
-    set(ECT_REGION_DEFECT, ph->sigma_defect >= 0 ? ph->sigma_defect : ph->sigma_tube,
-        kMu0 * (ph->mu_r_defect >= 0 ? ph->mu_r_defect : ph->mu_r_tube));
+    set(ECT_REGION_TSP, ph->sigma_tsp, kMu0 * ph->mu_r_tsp);
+    set(ECT_REGION_DEFECT, has_sd ? ph->sigma_defect : ph->sigma_tube,
+        kMu0 * (has_md ? ph->mu_r_defect : ph->mu_r_tube));
     set(ECT_REGION_COIL1, 0.0, kMu0);
     set(ECT_REGION_COIL2, 0.0, kMu0);
     set(ECT_REGION_VACUUM, 0.0, kMu0);
     if (ph->ibc_tsp) {
       // config.cpp:339-345: the plate volume is assembled as vacuum and
       // represented by the surface impedance of its material (materials.cpp:12-22)
-      const double s_tsp = ph->sigma_tsp >= 0 ? ph->sigma_tsp : 5e6;
-      const double mu_tsp = kMu0 * (ph->mu_r_tsp >= 0 ? ph->mu_r_tsp : 50.0);
-      require(m.omega > 0.0 && mu_tsp > 0.0 && s_tsp > 0.0, ECT_ERR_CONFIG,
-              "skin_depth requires positive omega, mu, sigma");
+      const double s_tsp = ph->sigma_tsp;
+      const double mu_tsp = kMu0 * ph->mu_r_tsp;
       const double delta = std::sqrt(2.0 / (m.omega * mu_tsp * s_tsp));
       const std::complex<double> z = std::complex<double>(1.0, -1.0) / (delta * s_tsp);
       m.ibc_enabled = 1;
@@ -483,28 +596,75 @@ int ect_matrix_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix** out) {
   });
 }
 
-int ect_matrix_from_csr(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* row_ptr,
-                        const int32_t* col_idx, const double* values, ect_matrix** out) {
+static int matrix_from_external(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* ptr,
+                                const int32_t* idx, const double* values, bool csc,
+                                ect_matrix** out) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     ScopedDevice sd(ctx->device);
-    require(n > 0 && nnz > 0 && nnz < (1ll << 31), ECT_ERR_SOLVER, "from_csr: bad dimensions");
+    require(n > 0 && nnz > 0 && nnz < (1ll << 31) && n < (1ll << 31), ECT_ERR_SOLVER,
+            csc ? "from_csc: bad dimensions" : "from_csr: bad dimensions");
+    require(ptr && idx && values, ECT_ERR_SOLVER, "matrix: null array");
     auto a = std::make_unique<ect_matrix>();
     a->ctx = ctx;
-    a->n = n;
-    a->nnz = nnz;
-    a->row_ptr.alloc(n + 1);
-    a->col.alloc(nnz);
-    a->val.alloc(nnz);
-    CK(cudaMemcpyAsync(a->row_ptr.p, row_ptr, (n + 1) * sizeof(int), cudaMemcpyDefault, ctx->stream));
-    CK(cudaMemcpyAsync(a->col.p, col_idx, nnz * sizeof(int), cudaMemcpyDefault, ctx->stream));
-    CK(cudaMemcpyAsync(a->val.p, values, nnz * sizeof(double2), cudaMemcpyDefault, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    a->assembled = true;
+    In<int> pi(ctx, ptr, n + 1);
+    In<int> ii(ctx, idx, nnz);
+    In<double2> vi(ctx, reinterpret_cast<const double2*>(values), nnz);
+    ect::matrix_from_compressed(ctx, n, nnz, pi.dev, ii.dev, vi.dev, csc, a.get());
     ect::compute_jacobi(a.get());
     if (ctx->use_sell) ect::build_sell(a.get(), ctx->sell_sigma);
     *out = a.release();
   });
+}
+
+int ect_matrix_from_csr(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* row_ptr,
+                        const int32_t* col_idx, const double* values, ect_matrix** out) {
+  return matrix_from_external(ctx, n, nnz, row_ptr, col_idx, values, false, out);
+}
+
+int ect_matrix_from_csc(ect_ctx* ctx, int64_t n, int64_t nnz, const int32_t* col_ptr,
+                        const int32_t* row_idx, const double* values, ect_matrix** out) {
+  return matrix_from_external(ctx, n, nnz, col_ptr, row_idx, values, true, out);
+}
+
+int ect_ctx_set_preconditioner(ect_ctx* ctx, int32_t precond) {
+  return guarded([&] {
+    require(precond == ECT_PRECOND_JACOBI || precond == ECT_PRECOND_AMG, ECT_ERR_CONFIG,
+            "unknown preconditioner");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ctx->precond = precond;
+  });
+}
+
+int ect_matrix_set_preconditioner(ect_matrix* m, int32_t precond) {
+  return guarded([&] {
+    require(precond == ECT_PRECOND_JACOBI || precond == ECT_PRECOND_AMG, ECT_ERR_CONFIG,
+            "unknown preconditioner");
+    std::lock_guard<std::recursive_mutex> lk(m->ctx->mu);
+    m->precond = precond;
+  });
+}
+
+int ect_matrix_precond_info(ect_matrix* m, double info[4]) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(m->ctx->mu);
+    ScopedDevice sd(m->ctx->device);
+    if (m->precond == ECT_PRECOND_AMG && m->symmetric && m->assembled && !m->amg)
+      ect::amg_setup(m);
+    if (m->precond != ECT_PRECOND_AMG || !m->amg) {
+      info[0] = 0.0;
+      info[1] = info[2] = info[3] = 0.0;
+      return;
+    }
+    info[0] = (double)m->amg->lv.size();
+    info[1] = m->amg->setup_ms;
+    info[2] = m->amg->op_complexity;
+    info[3] = (double)m->amg->lv.back().n;
+  });
+}
+
+int ect_matrix_symmetric(ect_matrix* m, int32_t* symmetric) {
+  return guarded([&] { *symmetric = m->symmetric ? 1 : 0; });
 }
 
 int ect_matrix_destroy(ect_matrix* a) {
@@ -528,6 +688,7 @@ int ect_matrix_assemble(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* mats,
     ScopedDevice sd(ctx->device);
     check_materials(*mats);
     EventTimer t(ctx, &ctx->timings.assemble_ms);
+    a->amg.reset();  // the multigrid hierarchy belongs to the old values
     ect::assemble_values(mesh, *mats, a);
   });
 }
@@ -583,6 +744,48 @@ int ect_rhs_coil(ect_ctx* ctx, ect_mesh* mesh, const ect_coil* coil, const doubl
   });
 }
 
+int ect_rhs_support(ect_ctx* ctx, ect_mesh* mesh, const int32_t* support_tets,
+                    int64_t n_support, double amplitude, double* rhs) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(n_support >= 0 && (n_support == 0 || support_tets), ECT_ERR_MESH,
+            "rhs: bad support list");
+    if (n_support == 0) ect::fail(ECT_ERR_MESH, "coil support is empty");
+    const size_t N = 3 * mesh->n_nodes + mesh->n_cond;
+    In<int> sup(ctx, support_tets, (size_t)n_support);
+    Out<double2> o(ctx, reinterpret_cast<double2*>(rhs), N);
+    EventTimer t(ctx, &ctx->timings.rhs_ms);
+    ect::build_rhs_support(mesh, sup.dev, n_support, -1, amplitude, o.dev);
+    o.finish();
+  });
+}
+
+int ect_rhs_region(ect_ctx* ctx, ect_mesh* mesh, int32_t coil_tag, double amplitude, double* rhs) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(coil_tag >= 0 && coil_tag < ECT_REGION_COUNT, ECT_ERR_MESH, "rhs: unknown region tag");
+    const size_t N = 3 * mesh->n_nodes + mesh->n_cond;
+    Out<double2> o(ctx, reinterpret_cast<double2*>(rhs), N);
+    EventTimer t(ctx, &ctx->timings.rhs_ms);
+    ect::build_rhs_support(mesh, nullptr, 0, coil_tag, amplitude, o.dev);
+    o.finish();
+  });
+}
+
+int ect_apply_pins_to_rhs(ect_ctx* ctx, ect_mesh* mesh, double* rhs, int32_t n_rhs) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    require(n_rhs >= 1, ECT_ERR_CONFIG, "apply_pins_to_rhs: n_rhs must be >= 1");
+    const size_t cnt = (size_t)(3 * mesh->n_nodes + mesh->n_cond) * n_rhs;
+    InOut<double2> io(ctx, reinterpret_cast<double2*>(rhs), cnt);
+    ect::apply_pins_rhs(mesh, io.dev, n_rhs);
+    io.finish();
+  });
+}
+
 int ect_spmv(ect_ctx* ctx, ect_matrix* a, const double* x, double* y, int32_t n_rhs) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
@@ -611,6 +814,7 @@ int ect_solve(ect_ctx* ctx, ect_matrix* a, const double* b, double* x, int32_t n
       EventTimer t(ctx, &ctx->timings.solve_ms);
       ect::cocg_solve(ctx, a, bi.dev, xo.dev, n_rhs, o, &so);
     }
+    ect::throw_on_breakdown(so);
     xo.finish();
     for (int c = 0; c < n_rhs; ++c) {
       results[c].iterations = so.iters[c];
@@ -717,6 +921,8 @@ struct ect_session {
   ect_iter_options opts{};
   ect_matrix* a_primary = nullptr;
   ect_matrix* a_reference = nullptr;
+  // right-hand sides and solutions of one batch, kept across calls
+  ect::DevBuf<double2> rhs, xp, xr;
   ~ect_session() {
     delete a_primary;
     delete a_reference;
@@ -783,7 +989,10 @@ int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
     const int64_t N = 3 * s->mesh->n_nodes + s->mesh->n_cond;
     const int P = positions_per_batch;
     const int kmax = 2 * P;
-    ect::DevBuf<double2> rhs((size_t)N * kmax), xp((size_t)N * kmax), xr((size_t)N * kmax);
+    s->rhs.ensure((size_t)N * kmax);
+    s->xp.ensure((size_t)N * kmax);
+    if (s->two_configs) s->xr.ensure((size_t)N * kmax);
+    auto &rhs = s->rhs, &xp = s->xp, &xr = s->xr;
     for (int p0 = 0; p0 < n_pos; p0 += P) {
       const int np = std::min(P, n_pos - p0);
       const int k = 2 * np;
@@ -811,6 +1020,8 @@ int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
           ect::cocg_solve(ctx, s->a_primary, rhs.p, xp.p, k, s->opts, &sp);
           if (s->two_configs) ect::cocg_solve(ctx, s->a_reference, rhs.p, xr.p, k, s->opts, &sr);
         }
+        // a failed solve (non-convergence or breakdown) fails its own position
+        // only (scan.cpp:111-114,139-141)
         for (int q = 0; q < np; ++q) {
           ect_signal_point& pt = pts[q];
           bool ok = sp.converged[2 * q] && sp.converged[2 * q + 1];

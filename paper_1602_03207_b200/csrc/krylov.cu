@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <thread>
 
@@ -140,7 +141,18 @@ __device__ __forceinline__ void reduce_partials(const double* partial, double (&
   block_sum<NV>(out, smem);
 }
 
-enum Mode { kPlain = 0, kCocg = 1, kResid = 2 };
+// SpMV epilogues:
+//  kPlain    : y = A x
+//  kCocg     : y = q = A p; per column p^T q (unconjugated) -> alpha = rho / p^T q
+//  kResid    : y = b - A x; per column ||y||^2 -> st.rnorm (true residual)
+//  kResidNR  : y = b - A x (multigrid residual, no reduction)
+//  kSmooth   : y = x + omega D^-1 (b - A x) (damped-Jacobi sweep, no reduction)
+//  kSmoothDot: kSmooth, plus per column b^T y (unconjugated) -> rho = r^T z of
+//              the preconditioned COCG (b = r, y = z = M r on the finest level)
+enum Mode { kPlain = 0, kCocg = 1, kResid = 2, kResidNR = 3, kSmooth = 4, kSmoothDot = 5 };
+__host__ __device__ constexpr int mode_nv(int mode, int k) {
+  return mode == kCocg || mode == kSmoothDot ? 2 * k : mode == kResid ? k : 0;
+}
 
 struct KrylovCtl {
   RhsState* st;       // [K]
@@ -157,6 +169,12 @@ struct KrylovCtl {
   int64_t s0, e0, s1, e1;
   // split SpMV (halo overlap): later launches add their totals into red
   int red_add;
+  // damped-Jacobi epilogues (kSmooth / kSmoothDot): D^-1 of the level, weight
+  const double2* dinv;
+  double omega;
+  // kSmoothDot: 1 = first preconditioned residual of a (re)start (sets rho),
+  // 0 = an iteration (beta = rho_new / rho)
+  int rho_start;
 };
 
 // ---- scalar finalisations (run by one thread on the global totals) ----------
@@ -206,6 +224,71 @@ __device__ void fin_update(const KrylovCtl& ctl, const double* tot) {
       s.rho = rho_new;
       ++active;
     }
+  }
+  *ctl.n_active = active;
+}
+
+// External preconditioner (multigrid): the update decides convergence from
+// ||r|| alone; rho = r^T z and beta come from the preconditioner's last
+// kernel (fin_rho).
+template <int K>
+__device__ void fin_update_norm(const KrylovCtl& ctl, const double* tot) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    s.xpend = s.status == kActive;
+    if (s.status != kActive) continue;
+    s.rnorm = sqrt(tot[k]);
+    s.iters += 1;
+    if (s.rnorm <= ctl.tol * s.bnorm) {
+      s.status = kConverged;
+    } else if (s.iters >= ctl.max_iter) {
+      s.status = kMaxIter;
+    } else {
+      ++active;
+    }
+  }
+  *ctl.n_active = active;
+}
+
+template <int K>
+__device__ void fin_rho(const KrylovCtl& ctl, const double* tot) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    if (s.status != kActive) continue;
+    const double2 rho_new = make_double2(tot[2 * k], tot[2 * k + 1]);
+    if (rho_new.x == 0.0 && rho_new.y == 0.0) {
+      s.status = kBreakdown;
+      continue;
+    }
+    if (!ctl.rho_start) s.beta = cdiv(rho_new, s.rho);
+    s.rho = rho_new;
+    ++active;
+  }
+  *ctl.n_active = active;
+}
+
+template <int K>
+__device__ void fin_start_norm(const KrylovCtl& ctl, const double* tot, unsigned mask,
+                               int fresh) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    if ((mask >> k) & 1u) {
+      if (fresh) {
+        s.bnorm = sqrt(tot[2 * k + 1]);
+        s.iters = 0;
+      }
+      s.rnorm = sqrt(tot[2 * k]);
+      if (fresh && s.bnorm == 0.0) s.status = kZeroRhs;
+      else if (s.rnorm <= ctl.tol * s.bnorm) s.status = kConverged;
+      else s.status = kActive;
+    }
+    active += s.status == kActive;
   }
   *ctl.n_active = active;
 }
@@ -265,8 +348,8 @@ __global__ void __launch_bounds__(kBlock)
 k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
        const double2* __restrict__ val, const double2* __restrict__ x, double2* __restrict__ y,
        const double2* __restrict__ b, KrylovCtl ctl) {
-  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
-  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  constexpr int NV0 = mode_nv(MODE, K), NV = NV0 > 0 ? NV0 : 1;
+  __shared__ double smem[32 * NV];
   if (MODE != kPlain && *ctl.n_active == 0) return;
   bool act[K];
 #pragma unroll
@@ -335,15 +418,27 @@ k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
           const double2 pv = x[idx];
           part[2 * k] += pv.x * acc[k].x - pv.y * acc[k].y;
           part[2 * k + 1] += pv.x * acc[k].y + pv.y * acc[k].x;
-        } else {
+        } else if (MODE == kResid) {
           const double2 rv = csub(b[idx], acc[k]);
           y[idx] = rv;
           part[k] += rv.x * rv.x + rv.y * rv.y;
+        } else if (MODE == kResidNR) {
+          y[idx] = csub(b[idx], acc[k]);
+        } else {
+          const double2 bv = b[idx];
+          const double2 zv = cadd(x[idx], cmul(make_double2(ctl.omega * ctl.dinv[row].x,
+                                                            ctl.omega * ctl.dinv[row].y),
+                                               csub(bv, acc[k])));
+          y[idx] = zv;
+          if (MODE == kSmoothDot) {
+            part[2 * k] += bv.x * zv.x - bv.y * zv.y;
+            part[2 * k + 1] += bv.x * zv.y + bv.y * zv.x;
+          }
         }
       }
     }
   }
-  if (MODE == kPlain) return;
+  if (NV0 == 0) return;
 
   block_sum<NV>(part, smem);
   if (threadIdx.x == 0)
@@ -358,6 +453,8 @@ k_spmv(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
       for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
     } else if (MODE == kCocg) {
       fin_alpha<K>(ctl, tot);
+    } else if (MODE == kSmoothDot) {
+      fin_rho<K>(ctl, tot);
     } else {
       fin_resid<K>(ctl, tot);
     }
@@ -459,8 +556,8 @@ k_sell_spmv(int64_t n_chunks, const int* __restrict__ off, const int* __restrict
             const int* __restrict__ scol, const double2* __restrict__ sval,
             const double2* __restrict__ x, double2* __restrict__ y, const double2* __restrict__ b,
             KrylovCtl ctl) {
-  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
-  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  constexpr int NV0 = mode_nv(MODE, K), NV = NV0 > 0 ? NV0 : 1;
+  __shared__ double smem[32 * NV];
   if (MODE != kPlain && *ctl.n_active == 0) return;
   bool act[K];
 #pragma unroll
@@ -502,15 +599,27 @@ k_sell_spmv(int64_t n_chunks, const int* __restrict__ off, const int* __restrict
           const double2 pv = x[idx];
           part[2 * k] += pv.x * acc[k].x - pv.y * acc[k].y;
           part[2 * k + 1] += pv.x * acc[k].y + pv.y * acc[k].x;
-        } else {
+        } else if (MODE == kResid) {
           const double2 rv = csub(b[idx], acc[k]);
           y[idx] = rv;
           part[k] += rv.x * rv.x + rv.y * rv.y;
+        } else if (MODE == kResidNR) {
+          y[idx] = csub(b[idx], acc[k]);
+        } else {
+          const double2 bv = b[idx];
+          const double2 zv = cadd(x[idx], cmul(make_double2(ctl.omega * ctl.dinv[row].x,
+                                                            ctl.omega * ctl.dinv[row].y),
+                                               csub(bv, acc[k])));
+          y[idx] = zv;
+          if (MODE == kSmoothDot) {
+            part[2 * k] += bv.x * zv.x - bv.y * zv.y;
+            part[2 * k + 1] += bv.x * zv.y + bv.y * zv.x;
+          }
         }
       }
     }
   }
-  if (MODE == kPlain) return;
+  if (NV0 == 0) return;
   block_sum<NV>(part, smem);
   if (threadIdx.x == 0)
 #pragma unroll
@@ -581,226 +690,9 @@ __global__ void k_sell_fill(int64_t n_slots, const int* __restrict__ perm,
 // narrow batch for a wide one (the CL lanes of one block load the same
 // addresses in the same instruction: one request), so wide batches keep the
 // software pipeline and 128-register occupancy instead of spilling.
-template <int G, int K, int MODE, int MINB = 1, int CL = 1>
-__global__ void __launch_bounds__(kBlock, MINB)
-k_nb_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
-          const double2* __restrict__ b, KrylovCtl ctl) {
-  static_assert(G % CL == 0 && K % CL == 0, "lane split");
-  constexpr int GB = G / CL;   // block lanes per node
-  constexpr int KL = K / CL;   // right-hand sides per lane
-  constexpr int NVL = (MODE == kCocg) ? 2 * KL : (MODE == kResid ? KL : 1);  // per lane
-  constexpr int NV = NVL * CL;
-  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
-  if (MODE != kPlain && *ctl.n_active == 0) return;
-  constexpr int NPW = 32 / G;  // nodes per warp and pass
-  const int lane = threadIdx.x & 31;
-  const int g = lane & (G - 1);
-  const int bl = g / CL, cl = g % CL;
-  const int kc = cl * KL;      // first column of this lane
-  bool act[KL];
-#pragma unroll
-  for (int k = 0; k < KL; ++k) act[k] = (MODE == kPlain) || ctl.st[kc + k].status == kActive;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t na = A.na;
-  double part[NVL];  // this lane's columns [kc, kc + KL)
-#pragma unroll
-  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
-
-  const int64_t w0 = A.node_begin & ~(int64_t)(NPW - 1);  // warps stay chunk-aligned
-  for (int64_t wn = w0 + warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
-    const int64_t i = wn + lane / G;
-    const bool valid = i >= A.node_begin && i < A.n_nodes;
-    double2 acc[3][KL], accv[KL];
-#pragma unroll
-    for (int k = 0; k < KL; ++k) {
-      acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
-    }
-    int cf_i = -1;
-    if (valid) {
-      const int be = A.blk_ptr[i + 1];
-      // software pipeline: the next block's column and planes are in flight
-      // while this block's x gathers and FMAs run (latency-bound otherwise)
-      int q = A.blk_ptr[i] + bl;
-      int m_nx = 0;
-      double B_nx[3][3], Im_nx[3];
-      if (q < be) {
-        m_nx = ldg_i(A.blk_col + q);
-        load_block(A, q, B_nx, Im_nx);
-      }
-      // (wide per-lane batches keep the accumulators instead)
-      constexpr bool kPipe = KL <= 2 && MINB <= 2;
-      for (; q < be; q += GB) {
-        int m = m_nx;
-        double B[3][3], Im[3];
-        if constexpr (kPipe) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            Im[c] = Im_nx[c];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
-          }
-          if (q + GB < be) {
-            m_nx = ldg_i(A.blk_col + q + GB);
-            load_block(A, q + GB, B_nx, Im_nx);
-          }
-        } else {
-          if (q != A.blk_ptr[i] + bl) {
-            m = ldg_i(A.blk_col + q);
-            load_block(A, q, B, Im);
-          } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              Im[c] = Im_nx[c];
-#pragma unroll
-              for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
-            }
-          }
-        }
-        const double2* xm = x + (int64_t)3 * m * K + kc;
-        // right-hand sides in pairs: one 256-bit gather per (component, pair)
-        constexpr int KP = (KL % 2 == 0) ? 2 : 1;
-#pragma unroll
-        for (int k0 = 0; k0 < KL; k0 += KP) {
-          if (!act[k0] && !act[k0 + KP - 1]) continue;
-          double2 xp[3][KP];
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            if constexpr (KP == 2) ld4x(xm + d * K + k0, xp[d][0], xp[d][1]);
-            else xp[d][0] = __ldg(xm + d * K + k0);
-          }
-#pragma unroll
-          for (int kk = 0; kk < KP; ++kk) {
-            const int k = k0 + kk;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              double2 s = acc[c][k];
-#pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                s.x += B[c][d] * xp[d][kk].x;
-                s.y += B[c][d] * xp[d][kk].y;
-              }
-              s.x -= Im[c] * xp[c][kk].y;
-              s.y += Im[c] * xp[c][kk].x;
-              acc[c][k] = s;
-            }
-          }
-        }
-      }
-      cf_i = A.cond_fwd[i];
-      if (cf_i >= 0) {
-        const int ce = A.cpl_ptr[i + 1];
-        for (int q = A.cpl_ptr[i] + bl; q < ce; q += GB) {
-          const int2 mi = ldg_i2(A.cpl_idx + q);
-          double av[3], va[3];
-          double2 Q3;
-          load_cpl(A, q, av, va, Q3);
-          const double2* xm = x + (int64_t)3 * mi.x * K + kc;
-          const double2* xvp = x + (na + mi.y) * K + kc;
-          constexpr int KP = (KL % 2 == 0) ? 2 : 1;
-#pragma unroll
-          for (int k0 = 0; k0 < KL; k0 += KP) {
-            if (!act[k0] && !act[k0 + KP - 1]) continue;
-            double2 xa[3][KP], xv[KP];
-            if constexpr (KP == 2) {
-              ld4x(xvp + k0, xv[0], xv[1]);
-#pragma unroll
-              for (int d = 0; d < 3; ++d) ld4x(xm + d * K + k0, xa[d][0], xa[d][1]);
-            } else {
-              xv[0] = __ldg(xvp + k0);
-#pragma unroll
-              for (int d = 0; d < 3; ++d) xa[d][0] = __ldg(xm + d * K + k0);
-            }
-#pragma unroll
-            for (int kk = 0; kk < KP; ++kk) {
-              const int k = k0 + kk;
-              const double2 v = xv[kk];
-#pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                acc[c][k].x += av[c] * v.x;
-                acc[c][k].y += av[c] * v.y;
-              }
-              double2 s = accv[k];
-#pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                s.x += va[d] * xa[d][kk].x;
-                s.y += va[d] * xa[d][kk].y;
-              }
-              s.x += Q3.x * v.x - Q3.y * v.y;
-              s.y += Q3.x * v.y + Q3.y * v.x;
-              accv[k] = s;
-            }
-          }
-        }
-      }
-    }
-    // segment reduction over the GB block lanes of a node (same column lane)
-#pragma unroll
-    for (int k = 0; k < KL; ++k) {
-#pragma unroll
-      for (int o = (GB / 2) * CL; o >= CL; o >>= 1) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
-          acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
-        }
-        accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
-        accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
-      }
-    }
-    if (bl == 0 && valid) {
-#pragma unroll
-      for (int k = 0; k < KL; ++k) {
-        if (!act[k]) continue;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c == 3 && cf_i < 0) break;
-          const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
-          const double2 v = c < 3 ? acc[c][k] : accv[k];
-          const int64_t idx = row * K + kc + k;
-          if (MODE == kPlain) {
-            y[idx] = v;
-          } else if (MODE == kCocg) {
-            y[idx] = v;
-            const double2 pv = x[idx];
-            part[2 * k] += pv.x * v.x - pv.y * v.y;
-            part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
-          } else {
-            const double2 rv = csub(b[idx], v);
-            y[idx] = rv;
-            part[k] += rv.x * rv.x + rv.y * rv.y;
-          }
-        }
-      }
-    }
-  }
-  if (MODE == kPlain) return;
-
-  // per-block totals, column-major over the lanes' slots = global column order
-  double bsum[NV];
-  block_sum_slots<NVL, CL>(part, smem, bsum);
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
-  if (!last_block(ctl.counter)) return;
-  double tot[NV];
-  reduce_partials<NV>(ctl.partial, tot, smem);
-  if (threadIdx.x == 0) {
-    if (ctl.red) {
-#pragma unroll
-      for (int j = 0; j < NV; ++j) ctl.red[j] = ctl.red_add ? ctl.red[j] + tot[j] : tot[j];
-    } else if (MODE == kCocg) {
-      fin_alpha<K>(ctl, tot);
-    } else {
-      fin_resid<K>(ctl, tot);
-    }
-    *ctl.counter = 0u;
-  }
-}
-
-// Same kernel over the sliced-ELL block layout (NB-E): chunks of 32 nodes,
+// NB SpMV over the sliced-ELL block layout (NB-E): chunks of 32 nodes,
 // block j of the chunk's nodes stored contiguously (1 KB per plane), padded to
-// the chunk's largest degree with zero blocks. A warp's block loads become
+// the chunk's largest degree with zero blocks. A warp's block loads are
 // contiguous runs instead of 16-32 scattered 64-byte pieces.
 template <int G, int K, int MODE, int MINB, int CL, int PFD = 0>
 __global__ void __launch_bounds__(kBlock, MINB)
@@ -809,9 +701,9 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   static_assert(G % CL == 0 && K % CL == 0, "lane split");
   constexpr int GB = G / CL;   // block lanes per node
   constexpr int KL = K / CL;   // right-hand sides per lane
-  constexpr int NVL = (MODE == kCocg) ? 2 * KL : (MODE == kResid ? KL : 1);  // per lane
+  constexpr int NVL0 = mode_nv(MODE, KL), NVL = NVL0 > 0 ? NVL0 : 1;  // per lane
   constexpr int NV = NVL * CL;
-  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
+  __shared__ double smem[32 * NV];
   if (MODE != kPlain && *ctl.n_active == 0) return;
   constexpr int NPW = 32 / G;  // nodes per warp and pass
   const int lane = threadIdx.x & 31;
@@ -1017,16 +909,28 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
             const double2 pv = x[idx];
             part[2 * k] += pv.x * v.x - pv.y * v.y;
             part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
-          } else {
+          } else if (MODE == kResid) {
             const double2 rv = csub(b[idx], v);
             y[idx] = rv;
             part[k] += rv.x * rv.x + rv.y * rv.y;
+          } else if (MODE == kResidNR) {
+            y[idx] = csub(b[idx], v);
+          } else {
+            const double2 bv = b[idx];
+            const double2 d = ctl.dinv[row];
+            const double2 zv = cadd(x[idx], cmul(make_double2(ctl.omega * d.x, ctl.omega * d.y),
+                                                 csub(bv, v)));
+            y[idx] = zv;
+            if (MODE == kSmoothDot) {
+              part[2 * k] += bv.x * zv.x - bv.y * zv.y;
+              part[2 * k + 1] += bv.x * zv.y + bv.y * zv.x;
+            }
           }
         }
       }
     }
   }
-  if (MODE == kPlain) return;
+  if (NVL0 == 0) return;
 
   // per-block totals, column-major over the lanes' slots = global column order
   double bsum[NV];
@@ -1043,576 +947,12 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       for (int j = 0; j < NV; ++j) ctl.red[j] = ctl.red_add ? ctl.red[j] + tot[j] : tot[j];
     } else if (MODE == kCocg) {
       fin_alpha<K>(ctl, tot);
+    } else if (MODE == kSmoothDot) {
+      fin_rho<K>(ctl, tot);
     } else {
       fin_resid<K>(ctl, tot);
     }
     *ctl.counter = 0u;
-  }
-}
-
-// ---- staged NB SpMV (NB-S): TMA bulk copies of the matrix stream -------------
-// The NB matrix stream of a group of NPW = 32 / G consecutive nodes is one
-// contiguous range of blocks [q0, q1) in each plane, so one elected lane per
-// warp moves it into a shared-memory ring slot with four cp.async.bulk copies
-// (3 planes + column indices) completing on an mbarrier, a group ahead of the
-// compute. The lanes then read their 3x3 blocks from shared memory; their
-// registers hold the x gathers one block ahead instead of in-flight matrix
-// loads (the register-pipelined kernel's limit for wide batches).
-constexpr int kSlots = 2;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n"
-      "DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// bytes of one ring slot for `cap` blocks (planes + columns), 128-B multiple
-__host__ __device__ inline size_t nbs_slot_bytes(int cap) {
-  return ((size_t)100 * cap + 127) & ~(size_t)127;
-}
-template <int NV, int NWARP>
-size_t nbs_smem(int cap) {
-  return (size_t)NWARP * kSlots * nbs_slot_bytes(cap) + NWARP * kSlots * sizeof(uint64_t) +
-         32 * NV * sizeof(double);
-}
-
-template <int G, int K, int MODE, int CL, int NWARP>
-__global__ void __launch_bounds__(NWARP * 32, 1)
-k_nbs_spmv(NbView A, int cap, const double2* __restrict__ x, double2* __restrict__ y,
-           const double2* __restrict__ b, KrylovCtl ctl) {
-  static_assert(G % CL == 0 && K % CL == 0, "lane split");
-  constexpr int GB = G / CL;
-  constexpr int KL = K / CL;
-  constexpr int NVL = (MODE == kCocg) ? 2 * KL : (MODE == kResid ? KL : 1);
-  constexpr int NV = NVL * CL;
-  constexpr int NPW = 32 / G;
-  extern __shared__ __align__(128) unsigned char sm_raw[];
-  if (MODE != kPlain && *ctl.n_active == 0) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int g = lane & (G - 1);
-  const int bl = g / CL, cl = g % CL;
-  const int kc = cl * KL;
-  const size_t slot_bytes = nbs_slot_bytes(cap);
-  unsigned char* ring = sm_raw + (size_t)wid * kSlots * slot_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + (size_t)NWARP * kSlots * slot_bytes) +
-                   wid * kSlots;
-  double* red = reinterpret_cast<double*>(bars - wid * kSlots + NWARP * kSlots);
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  bool act[KL];
-#pragma unroll
-  for (int k = 0; k < KL; ++k) act[k] = (MODE == kPlain) || ctl.st[kc + k].status == kActive;
-  const int64_t na = A.na;
-  const int64_t n_groups = (A.n_nodes + NPW - 1) / NPW;
-  const int64_t gstride = (int64_t)gridDim.x * NWARP;
-  double part[NVL];
-#pragma unroll
-  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
-
-  auto issue = [&](int64_t grp, int s) {
-    if (lane == 0) {
-      const int64_t n0 = grp * NPW;
-      const int64_t n1 = n0 + NPW < A.n_nodes ? n0 + NPW : A.n_nodes;
-      const int qa = A.blk_ptr[n0] & ~3, qb = (A.blk_ptr[n1] + 3) & ~3;
-      const int nq = qb - qa;
-      unsigned char* slot = ring + (size_t)s * slot_bytes;
-      mbar_expect_tx(&bars[s], 100u * nq);
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-        bulk_g2s(slot + (size_t)p * cap * 32, A.blk + 4 * ((int64_t)p * A.nblk + qa), 32u * nq,
-                 &bars[s]);
-      bulk_g2s(slot + (size_t)3 * cap * 32, A.blk_col + qa, 4u * nq, &bars[s]);
-    }
-  };
-
-  unsigned phase = 0;
-  int s = 0;
-  int64_t grp = blockIdx.x * (int64_t)NWARP + wid;
-  if (grp < n_groups) issue(grp, 0);
-  for (; grp < n_groups; grp += gstride) {
-    __syncwarp();  // every lane is done with slot s ^ 1 (consumed last iteration)
-    if (grp + gstride < n_groups) issue(grp + gstride, s ^ 1);
-    mbar_wait(&bars[s], (phase >> s) & 1u);
-    phase ^= 1u << s;
-    const unsigned char* slot = ring + (size_t)s * slot_bytes;
-    const double* P0 = reinterpret_cast<const double*>(slot);
-    const double* P1 = P0 + 4 * cap;
-    const double* P2 = P0 + 8 * cap;
-    const int* col = reinterpret_cast<const int*>(slot + (size_t)3 * cap * 32);
-
-    const int64_t i = grp * NPW + lane / G;
-    const bool valid = i < A.n_nodes;
-    double2 acc[3][KL], accv[KL];
-#pragma unroll
-    for (int k = 0; k < KL; ++k) acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
-    int cf_i = -1;
-    if (valid) {
-      const int qa = A.blk_ptr[grp * NPW] & ~3;
-      const int je = A.blk_ptr[i + 1] - qa;
-      int j = A.blk_ptr[i] - qa + bl;
-      double2 xc[3][KL];
-      if (j < je) {
-        const double2* xm = x + (int64_t)3 * col[j] * K + kc;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) load_xk<KL>(xm + d * K, xc[d]);
-      }
-      for (; j < je; j += GB) {
-        // gathers of the next block in flight while this block's FMAs run
-        double2 xn[3][KL];
-        if (j + GB < je) {
-          const double2* xm = x + (int64_t)3 * col[j + GB] * K + kc;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) load_xk<KL>(xm + d * K, xn[d]);
-        }
-        const double4 v0 = *reinterpret_cast<const double4*>(P0 + 4 * j);
-        const double4 v1 = *reinterpret_cast<const double4*>(P1 + 4 * j);
-        const double4 v2 = *reinterpret_cast<const double4*>(P2 + 4 * j);
-        const double B[3][3] = {{v0.x, v0.y, v0.z}, {v0.w, v1.x, v1.y}, {v1.z, v1.w, v2.x}};
-        const double Im[3] = {v2.y, v2.z, v2.w};
-#pragma unroll
-        for (int k = 0; k < KL; ++k) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            double2 t = acc[c][k];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              t.x += B[c][d] * xc[d][k].x;
-              t.y += B[c][d] * xc[d][k].y;
-            }
-            t.x -= Im[c] * xc[c][k].y;
-            t.y += Im[c] * xc[c][k].x;
-            acc[c][k] = t;
-          }
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int k = 0; k < KL; ++k) xc[d][k] = xn[d][k];
-      }
-      cf_i = A.cond_fwd[i];
-      if (cf_i >= 0) {
-        const int ce = A.cpl_ptr[i + 1];
-        for (int q = A.cpl_ptr[i] + bl; q < ce; q += GB) {
-          const int2 mi = ldg_i2(A.cpl_idx + q);
-          double av[3], va[3];
-          double2 Q3;
-          load_cpl(A, q, av, va, Q3);
-          const double2* xm = x + (int64_t)3 * mi.x * K + kc;
-          const double2* xvp = x + (na + mi.y) * K + kc;
-          constexpr int KP = KL % 2 == 0 ? 2 : 1;
-#pragma unroll
-          for (int k0 = 0; k0 < KL; k0 += KP) {
-            double2 xa[3][KP], xv[KP];
-            load_xk<KP>(xvp + k0, xv);
-#pragma unroll
-            for (int d = 0; d < 3; ++d) load_xk<KP>(xm + d * K + k0, xa[d]);
-#pragma unroll
-            for (int kk = 0; kk < KP; ++kk) {
-              const int k = k0 + kk;
-              const double2 v = xv[kk];
-#pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                acc[c][k].x += av[c] * v.x;
-                acc[c][k].y += av[c] * v.y;
-              }
-              double2 t = accv[k];
-#pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                t.x += va[d] * xa[d][kk].x;
-                t.y += va[d] * xa[d][kk].y;
-              }
-              t.x += Q3.x * v.x - Q3.y * v.y;
-              t.y += Q3.x * v.y + Q3.y * v.x;
-              accv[k] = t;
-            }
-          }
-        }
-      }
-    }
-    s ^= 1;
-    // segment reduction over the GB block lanes of a node (same column lane)
-#pragma unroll
-    for (int k = 0; k < KL; ++k) {
-#pragma unroll
-      for (int o = (GB / 2) * CL; o >= CL; o >>= 1) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
-          acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
-        }
-        accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
-        accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
-      }
-    }
-    if (bl == 0 && valid) {
-#pragma unroll
-      for (int k = 0; k < KL; ++k) {
-        if (!act[k]) continue;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c == 3 && cf_i < 0) break;
-          const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
-          const double2 v = c < 3 ? acc[c][k] : accv[k];
-          const int64_t idx = row * K + kc + k;
-          if (MODE == kPlain) {
-            y[idx] = v;
-          } else if (MODE == kCocg) {
-            y[idx] = v;
-            const double2 pv = x[idx];
-            part[2 * k] += pv.x * v.x - pv.y * v.y;
-            part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
-          } else {
-            const double2 rv = csub(b[idx], v);
-            y[idx] = rv;
-            part[k] += rv.x * rv.x + rv.y * rv.y;
-          }
-        }
-      }
-    }
-  }
-  if (MODE == kPlain) return;
-
-  double bsum[NV];
-  block_sum_slots<NVL, CL>(part, red, bsum);
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
-  if (!last_block(ctl.counter)) return;
-  double tot[NV];
-  reduce_partials<NV>(ctl.partial, tot, red);
-  if (threadIdx.x == 0) {
-    if (ctl.red) {
-#pragma unroll
-      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
-    } else if (MODE == kCocg) {
-      fin_alpha<K>(ctl, tot);
-    } else {
-      fin_resid<K>(ctl, tot);
-    }
-    *ctl.counter = 0u;
-  }
-}
-
-// max over node groups of the padded block count of one ring slot
-__global__ void k_nbs_cap(const int* __restrict__ blk_ptr, int64_t n_nodes, int npw,
-                          int* __restrict__ cap) {
-  const int64_t ng = (n_nodes + npw - 1) / npw;
-  int best = 0;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t n0 = g * npw, n1 = n0 + npw < n_nodes ? n0 + npw : n_nodes;
-    const int nq = ((blk_ptr[n1] + 3) & ~3) - (blk_ptr[n0] & ~3);
-    best = nq > best ? nq : best;
-  }
-  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(cap, best);
-}
-
-// ---- tiled NB SpMV with shared-memory x staging (NB-T) -------------------------
-// A CTA owns a tile of kTileW consecutive nodes. The union of their neighbour
-// nodes (the tile's x "footprint", ~7 runs of consecutive node ids on a
-// lexicographically numbered mesh, ~0.5 of the per-block gathers) is staged
-// once into shared memory with coalesced loads; blocks then address x through
-// a 16-bit local column. This replaces ~15 scattered 96-byte x gathers per
-// node (the L1-wavefront bottleneck of the untiled kernel) by ~7 coalesced
-// ones, and shrinks the per-block column from 4 to 2 bytes.
-constexpr int kTileW = 64;
-
-struct NbtView {
-  NbView nb;
-  const int* fp_off;       // ntiles + 1
-  const int* fp_node;      // footprint node ids, sorted per tile
-  const uint16_t* lcol;    // per block: index in its tile's footprint
-  const uint16_t* cpl_lcol;  // per coupling: index of m in the footprint
-  int64_t ntiles;
-  int fmax;
-};
-
-template <int K, int MODE>
-__global__ void __launch_bounds__(kBlock, 2)
-k_nbt_spmv(NbtView T, const double2* __restrict__ x, double2* __restrict__ y,
-           const double2* __restrict__ b, KrylovCtl ctl) {
-  constexpr int G = 4;
-  constexpr int NV = (MODE == kCocg) ? 2 * K : (MODE == kResid ? K : 1);
-  constexpr int S = 4 * K + 1;  // double2 per staged node: 3K (A) + K (V) + 1 pad (banks)
-  extern __shared__ double2 sx[];
-  __shared__ double smem[32 * (NV > 0 ? NV : 1)];
-  if (MODE != kPlain && *ctl.n_active == 0) return;
-  bool act[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) act[k] = (MODE == kPlain) || ctl.st[k].status == kActive;
-  const NbView& A = T.nb;
-  const int lane = threadIdx.x & 31;
-  const int g = lane & (G - 1);
-  const int64_t na = A.na;
-  double part[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) part[j] = 0.0;
-
-  for (int64_t t = blockIdx.x; t < T.ntiles; t += gridDim.x) {
-    const int f0 = T.fp_off[t], F = T.fp_off[t + 1] - f0;
-    __syncthreads();  // previous tile's readers are done
-    for (int e = threadIdx.x; e < F * 3 * K; e += blockDim.x) {
-      const int f = e / (3 * K), c = e - f * (3 * K);
-      sx[f * S + c] = x[(int64_t)T.fp_node[f0 + f] * 3 * K + c];
-    }
-    for (int e = threadIdx.x; e < F * K; e += blockDim.x) {
-      const int f = e / K, k = e - f * K;
-      const int cfm = A.cond_fwd[T.fp_node[f0 + f]];
-      sx[f * S + 3 * K + k] = cfm >= 0 ? x[(na + cfm) * K + k] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    for (int jb = 0; jb < kTileW; jb += kBlock / G) {
-      const int64_t i = t * kTileW + jb + threadIdx.x / G;
-      const bool valid = i < A.n_nodes;
-      double2 acc[3][K], accv[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
-      int cf_i = -1;
-      if (valid) {
-        const int be = A.blk_ptr[i + 1];
-        int q = A.blk_ptr[i] + g;
-        int l_nx = 0;
-        double B_nx[3][3], Im_nx[3];
-        if (q < be) {
-          l_nx = T.lcol[q];
-          load_block(A, q, B_nx, Im_nx);
-        }
-        for (; q < be; q += G) {
-          const int l = l_nx;
-          double B[3][3], Im[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            Im[c] = Im_nx[c];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
-          }
-          if (q + G < be) {
-            l_nx = T.lcol[q + G];
-            load_block(A, q + G, B_nx, Im_nx);
-          }
-          const double2* xm = sx + l * S;
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (!act[k]) continue;
-            const double2 xs[3] = {xm[k], xm[K + k], xm[2 * K + k]};
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              double2 s = acc[c][k];
-#pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                s.x += B[c][d] * xs[d].x;
-                s.y += B[c][d] * xs[d].y;
-              }
-              s.x -= Im[c] * xs[c].y;
-              s.y += Im[c] * xs[c].x;
-              acc[c][k] = s;
-            }
-          }
-        }
-        cf_i = A.cond_fwd[i];
-        if (cf_i >= 0) {
-          const int ce = A.cpl_ptr[i + 1];
-          for (int q = A.cpl_ptr[i] + g; q < ce; q += G) {
-            const int l = T.cpl_lcol[q];
-            double av[3], va[3];
-            double2 Q3;
-            load_cpl(A, q, av, va, Q3);
-            const double2* xm = sx + l * S;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (!act[k]) continue;
-              const double2 v = xm[3 * K + k];
-#pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                acc[c][k].x += av[c] * v.x;
-                acc[c][k].y += av[c] * v.y;
-              }
-              double2 s = accv[k];
-#pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                const double2 xd = xm[d * K + k];
-                s.x += va[d] * xd.x;
-                s.y += va[d] * xd.y;
-              }
-              s.x += Q3.x * v.x - Q3.y * v.y;
-              s.y += Q3.x * v.y + Q3.y * v.x;
-              accv[k] = s;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-#pragma unroll
-        for (int o = G / 2; o; o >>= 1) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
-            acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
-          }
-          accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
-          accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
-        }
-      }
-      if (g == 0 && valid) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if (!act[k]) continue;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (c == 3 && cf_i < 0) break;
-            const int64_t row = c < 3 ? 3 * i + c : na + cf_i;
-            const double2 v = c < 3 ? acc[c][k] : accv[k];
-            const int64_t idx = row * K + k;
-            if (MODE == kPlain) {
-              y[idx] = v;
-            } else if (MODE == kCocg) {
-              y[idx] = v;
-              const double2 pv = x[idx];
-              part[2 * k] += pv.x * v.x - pv.y * v.y;
-              part[2 * k + 1] += pv.x * v.y + pv.y * v.x;
-            } else {
-              const double2 rv = csub(b[idx], v);
-              y[idx] = rv;
-              part[k] += rv.x * rv.x + rv.y * rv.y;
-            }
-          }
-        }
-      }
-    }
-  }
-  if (MODE == kPlain) return;
-
-  block_sum<NV>(part, smem);
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = part[j];
-  if (!last_block(ctl.counter)) return;
-  double tot[NV];
-  reduce_partials<NV>(ctl.partial, tot, smem);
-  if (threadIdx.x == 0) {
-    if (ctl.red) {
-#pragma unroll
-      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
-    } else if (MODE == kCocg) {
-      fin_alpha<K>(ctl, tot);
-    } else {
-      fin_resid<K>(ctl, tot);
-    }
-    *ctl.counter = 0u;
-  }
-}
-
-// Tile footprints: CTA per tile sorts the tile's block columns in shared
-// memory (bitonic), dedupes, and (write pass) emits the footprint and the
-// 16-bit local columns. kMaxTileCols bounds the per-tile block count.
-constexpr int kMaxTileCols = 4096;
-
-__global__ void __launch_bounds__(512)
-k_tile_footprint(const int* __restrict__ blk_ptr, const int* __restrict__ blk_col,
-                 const int* __restrict__ cpl_ptr, const int2* __restrict__ cpl_idx,
-                 int64_t n_nodes, int64_t ntiles, int write, const int* __restrict__ fp_off,
-                 int* fp_count, int* fp_node, uint16_t* lcol, uint16_t* cpl_lcol, int* bad) {
-  __shared__ int keys[kMaxTileCols];
-  __shared__ int uniq_cnt;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t i0 = t * kTileW;
-    const int64_t i1 = n_nodes < i0 + kTileW ? n_nodes : i0 + kTileW;
-    const int q0 = blk_ptr[i0], q1 = blk_ptr[i1];
-    const int C = q1 - q0;
-    if (C > kMaxTileCols) {
-      if (threadIdx.x == 0) atomicOr(bad, 1);
-      continue;
-    }
-    int P = 1;
-    while (P < C) P <<= 1;
-    __syncthreads();
-    for (int e = threadIdx.x; e < P; e += blockDim.x) keys[e] = e < C ? blk_col[q0 + e] : INT_MAX;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int e = threadIdx.x; e < P; e += blockDim.x) {
-          const int o = e ^ j;
-          if (o > e) {
-            const bool up = (e & k) == 0;
-            const int a = keys[e], bb = keys[o];
-            if ((a > bb) == up) {
-              keys[e] = bb;
-              keys[o] = a;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    // compact uniques in place (serial over P by one warp would be slow; use a
-    // two-step: mark heads, then thread 0 compacts — C is small)
-    if (threadIdx.x == 0) {
-      int u = 0;
-      for (int e = 0; e < C; ++e)
-        if (e == 0 || keys[e] != keys[e - 1]) keys[u++] = keys[e];
-      uniq_cnt = u;
-    }
-    __syncthreads();
-    const int U = uniq_cnt;
-    if (!write) {
-      if (threadIdx.x == 0) {
-        fp_count[t] = U;
-        if (U > 65535) atomicOr(bad, 1);
-      }
-      continue;
-    }
-    const int f0 = fp_off[t];
-    for (int e = threadIdx.x; e < U; e += blockDim.x) fp_node[f0 + e] = keys[e];
-    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-      const int m = blk_col[q];
-      int lo = 0, hi = U - 1;
-      while (lo < hi) {
-        const int mid = lo + ((hi - lo) >> 1);
-        if (keys[mid] < m) lo = mid + 1; else hi = mid;
-      }
-      lcol[q] = (uint16_t)lo;
-    }
-    const int c0 = cpl_ptr[i0], c1 = cpl_ptr[i1];
-    for (int q = c0 + threadIdx.x; q < c1; q += blockDim.x) {
-      const int m = cpl_idx[q].x;
-      int lo = 0, hi = U - 1;
-      while (lo < hi) {
-        const int mid = lo + ((hi - lo) >> 1);
-        if (keys[mid] < m) lo = mid + 1; else hi = mid;
-      }
-      cpl_lcol[q] = (uint16_t)lo;
-    }
   }
 }
 
@@ -1755,12 +1095,15 @@ struct VecMap {
 // r -= alpha q ; z = D^-1 r ; partial r^T z, ||r||^2
 // last block: convergence test, beta, rho. The iteration's x += alpha p is
 // deferred to k_pupdate, which reads p anyway (x and p travel once, not twice).
-template <int K>
+// EXT (external preconditioner, multigrid): partial ||r||^2 only; rho and beta
+// come from the preconditioner's last kernel (kSmoothDot).
+template <int K, bool EXT = false>
 __global__ void __launch_bounds__(kBlock)
 k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
          const double2* __restrict__ dinv, KrylovCtl ctl) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
-  constexpr int NVL = 3 * CW, NV = 3 * K;
+  constexpr int PV = EXT ? 1 : 3;  // values per column
+  constexpr int NVL = PV * CW, NV = PV * K;
   __shared__ double smem[32 * NV];
   if (*ctl.n_active == 0) return;
   const int h = (threadIdx.x & 31) % KH, kb = h * CW;
@@ -1779,17 +1122,21 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
-    const double2 d = dinv[i];
+    const double2 d = EXT ? make_double2(0.0, 0.0) : dinv[i];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
       if (!act[c]) continue;
       const int64_t idx = i * K + kb + c;
       const double2 rv = csub(r[idx], cmul(alpha[c], q[idx]));
       r[idx] = rv;
-      const double2 z = cmul(d, rv);
-      part[3 * c] += rv.x * z.x - rv.y * z.y;
-      part[3 * c + 1] += rv.x * z.y + rv.y * z.x;
-      part[3 * c + 2] += rv.x * rv.x + rv.y * rv.y;
+      if constexpr (EXT) {
+        part[c] += rv.x * rv.x + rv.y * rv.y;
+      } else {
+        const double2 z = cmul(d, rv);
+        part[3 * c] += rv.x * z.x - rv.y * z.y;
+        part[3 * c + 1] += rv.x * z.y + rv.y * z.x;
+        part[3 * c + 2] += rv.x * rv.x + rv.y * rv.y;
+      }
     }
   }
   double bsum[NV];
@@ -1804,6 +1151,8 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
     if (ctl.red) {
 #pragma unroll
       for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (EXT) {
+      fin_update_norm<K>(ctl, tot);
     } else {
       fin_update<K>(ctl, tot);
     }
@@ -1811,11 +1160,13 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
   }
 }
 
-// x += alpha p (owed by the last k_update) ; p = D^-1 r + beta p (active columns)
-template <int K>
+// x += alpha p (owed by the last k_update) ; p = z + beta p (active columns),
+// z = D^-1 r (Jacobi) or the preconditioner's output zv (EXT)
+template <int K, bool EXT = false>
 __global__ void __launch_bounds__(kBlock)
 k_pupdate(int64_t n, double2* __restrict__ x, const double2* __restrict__ r,
-          double2* __restrict__ p, const double2* __restrict__ dinv, KrylovCtl ctl) {
+          double2* __restrict__ p, const double2* __restrict__ dinv, KrylovCtl ctl,
+          const double2* __restrict__ zv = nullptr) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
   bool any = *ctl.n_active != 0;
 #pragma unroll
@@ -1837,14 +1188,14 @@ k_pupdate(int64_t n, double2* __restrict__ x, const double2* __restrict__ r,
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
-    const double2 d = dinv[i];
+    const double2 d = EXT ? make_double2(0.0, 0.0) : dinv[i];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
       if (!act[c] && !xp[c]) continue;
       const int64_t idx = i * K + kb + c;
       const double2 pv = p[idx];
       if (xp[c]) x[idx] = cadd(x[idx], cmul(alpha[c], pv));
-      if (act[c]) p[idx] = cadd(cmul(d, r[idx]), cmul(beta[c], pv));
+      if (act[c]) p[idx] = cadd(EXT ? zv[idx] : cmul(d, r[idx]), cmul(beta[c], pv));
     }
   }
   // the owed updates are done: clear the flags (after every block read them)
@@ -1858,14 +1209,16 @@ k_pupdate(int64_t n, double2* __restrict__ x, const double2* __restrict__ r,
 
 // (Re)start selected columns from their residual r: p = D^-1 r, rho = r^T z,
 // ||r||; on a fresh start also x = 0, r = b and bnorm = ||b||.
-// mask bit k set -> (re)start column k.
-template <int K>
+// mask bit k set -> (re)start column k. EXT: norms only (p and rho come from
+// the preconditioner applied next).
+template <int K, bool EXT = false>
 __global__ void __launch_bounds__(kBlock)
 k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, double2* __restrict__ r,
         double2* __restrict__ p, const double2* __restrict__ dinv, unsigned mask, int fresh,
         KrylovCtl ctl) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
-  constexpr int NVL = 4 * CW, NV = 4 * K;
+  constexpr int PV = EXT ? 2 : 4;
+  constexpr int NVL = PV * CW, NV = PV * K;
   __shared__ double smem[32 * NV];
   const int h = (threadIdx.x & 31) % KH, kb = h * CW;
   double part[NVL];
@@ -1876,7 +1229,7 @@ k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, doubl
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
-    const double2 d = dinv[i];
+    const double2 d = EXT ? make_double2(0.0, 0.0) : dinv[i];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
       if (!((mask >> (kb + c)) & 1u)) continue;
@@ -1886,15 +1239,19 @@ k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, doubl
         rv = b[idx];
         x[idx] = make_double2(0.0, 0.0);
         r[idx] = rv;
-        part[4 * c + 3] += rv.x * rv.x + rv.y * rv.y;
+        part[PV * c + PV - 1] += rv.x * rv.x + rv.y * rv.y;
       } else {
         rv = r[idx];
       }
-      const double2 z = cmul(d, rv);
-      p[idx] = z;
-      part[4 * c] += rv.x * z.x - rv.y * z.y;
-      part[4 * c + 1] += rv.x * z.y + rv.y * z.x;
-      part[4 * c + 2] += rv.x * rv.x + rv.y * rv.y;
+      if constexpr (EXT) {
+        part[2 * c] += rv.x * rv.x + rv.y * rv.y;
+      } else {
+        const double2 z = cmul(d, rv);
+        p[idx] = z;
+        part[4 * c] += rv.x * z.x - rv.y * z.y;
+        part[4 * c + 1] += rv.x * z.y + rv.y * z.x;
+        part[4 * c + 2] += rv.x * rv.x + rv.y * rv.y;
+      }
     }
   }
   double bsum[NV];
@@ -1909,6 +1266,8 @@ k_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x, doubl
     if (ctl.red) {
 #pragma unroll
       for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (EXT) {
+      fin_start_norm<K>(ctl, tot, mask, fresh);
     } else {
       fin_start<K>(ctl, tot, mask, fresh);
     }
@@ -1949,240 +1308,93 @@ NbView nb_view(const ect_matrix* a) {
                 a->n_nodes, 3 * a->n_nodes};
 }
 
-constexpr size_t kNbtMaxSmem = 110 * 1024;
-
-NbtView nbt_view(const ect_matrix* a) {
-  return NbtView{nb_view(a), a->nbt_fp_off.p, a->nbt_fp_node.p, a->nbt_lcol.p,
-                 a->nbt_cpl_lcol.p, a->nbt_tiles, a->nbt_fmax};
-}
-
-template <int K>
-size_t nbt_smem(const ect_matrix* a) {
-  return (size_t)a->nbt_fmax * (4 * K + 1) * sizeof(double2);
-}
-
+// Default NB-E launch configuration per batch width (measured on configs[1],
+// B200): G lanes per node, CTAs per SM, CL column lanes, L2 prefetch distance.
 template <int K, int MODE>
-const void* nbt_fn() {
-  return (const void*)k_nbt_spmv<K, MODE>;
+const void* nbe_kernel() {
+  if constexpr (K <= 2) return (const void*)k_nbe_spmv<2, K, MODE, 2, 1, 2>;
+  else if constexpr (K == 4) return (const void*)k_nbe_spmv<2, K, MODE, 2, 2, 4>;
+  else if constexpr (K == 8) return (const void*)k_nbe_spmv<4, K, MODE, 2, 4, 4>;
+  else return (const void*)k_nbe_spmv<8, K, MODE, 2, 8>;
 }
-
-// NB kernel variant: lanes per node G and the occupancy target MINB
-// (ECT_NB_VARIANT, read at context creation; 0 is the default).
 template <int K>
-const void* nb_fn(int variant, int mode) {
-#define ECT_NBF(G_, MB_, CL_)                                                   \
-  (mode == kPlain  ? (const void*)k_nb_spmv<G_, K, kPlain, MB_, CL_>            \
-   : mode == kCocg ? (const void*)k_nb_spmv<G_, K, kCocg, MB_, CL_>             \
-                   : (const void*)k_nb_spmv<G_, K, kResid, MB_, CL_>)
-  // Measured on B200 (configs[1]): 2 block lanes per node with <= 2
-  // right-hand sides per lane (column lanes for wider batches), 2 CTAs/SM.
-  if constexpr (K <= 2) {
-    switch (variant) {
-      case 1: return ECT_NBF(4, 1, 1);
-      case 4: return ECT_NBF(8, 2, 1);
-      case 9: return ECT_NBF(1, 2, 1);
-      default: return ECT_NBF(2, 2, 1);
-    }
-  } else if constexpr (K == 4) {
-    switch (variant) {
-      case 7: return ECT_NBF(2, 2, 1);   // 2 block lanes x 4 columns (spills)
-      case 15: return ECT_NBF(4, 2, 2);  // 2 block lanes x 2 column lanes
-      default: return ECT_NBF(2, 2, 2);  // 1 block lane x 2 column lanes
-    }
-  } else if constexpr (K == 8) {
-    switch (variant) {
-      case 16: return ECT_NBF(8, 1, 1);
-      case 17: return ECT_NBF(8, 2, 4);  // 2 block lanes x 4 column lanes
-      default: return ECT_NBF(4, 2, 4);  // 1 block lane x 4 column lanes
-    }
-  } else {
-    return ECT_NBF(8, 2, 8);
+const void* nbe_fn(int mode) {
+  switch (mode) {
+    case kPlain: return nbe_kernel<K, kPlain>();
+    case kCocg: return nbe_kernel<K, kCocg>();
+    case kResid: return nbe_kernel<K, kResid>();
+    case kResidNR: return nbe_kernel<K, kResidNR>();
+    case kSmooth: return nbe_kernel<K, kSmooth>();
+    default: return nbe_kernel<K, kSmoothDot>();
   }
-#undef ECT_NBF
 }
-
 template <int K>
-const void* nbe_fn(int variant, int mode) {
-#define ECT_NBE(G_, MB_, CL_)                                                   \
-  (mode == kPlain  ? (const void*)k_nbe_spmv<G_, K, kPlain, MB_, CL_>            \
-   : mode == kCocg ? (const void*)k_nbe_spmv<G_, K, kCocg, MB_, CL_>             \
-                   : (const void*)k_nbe_spmv<G_, K, kResid, MB_, CL_>)
-#define ECT_NBEP(G_, MB_, CL_, PF_)                                             \
-  (mode == kPlain  ? (const void*)k_nbe_spmv<G_, K, kPlain, MB_, CL_, PF_>       \
-   : mode == kCocg ? (const void*)k_nbe_spmv<G_, K, kCocg, MB_, CL_, PF_>        \
-                   : (const void*)k_nbe_spmv<G_, K, kResid, MB_, CL_, PF_>)
-  if constexpr (K <= 2) {
-    switch (variant) {
-      case 51: return ECT_NBE(4, 2, 1);
-      case 53: return ECT_NBEP(2, 2, 1, 2);
-      case 54: return ECT_NBEP(2, 2, 1, 4);
-      case 55: return ECT_NBEP(2, 2, 1, 8);
-      case 56: return ECT_NBE(2, 2, 1);
-      default: return ECT_NBEP(2, 2, 1, 2);  // measured best (configs[1], B200)
-    }
-  } else if constexpr (K == 4) {
-    switch (variant) {
-      case 51: return ECT_NBE(4, 2, 2);
-      case 53: return ECT_NBEP(2, 2, 2, 2);
-      case 54: return ECT_NBEP(2, 2, 2, 4);
-      case 55: return ECT_NBEP(2, 2, 2, 8);
-      case 56: return ECT_NBE(2, 2, 2);
-      default: return ECT_NBEP(2, 2, 2, 4);
-    }
-  } else if constexpr (K == 8) {
-    switch (variant) {
-      case 51: return ECT_NBE(8, 2, 4);
-      case 53: return ECT_NBEP(4, 2, 4, 2);
-      case 54: return ECT_NBEP(4, 2, 4, 4);
-      case 55: return ECT_NBEP(4, 2, 4, 8);
-      case 56: return ECT_NBE(4, 2, 4);
-      default: return ECT_NBEP(4, 2, 4, 4);
-    }
-  } else {
-    return ECT_NBE(8, 2, 8);
+const void* csr_fn(int mode) {
+  constexpr int G = K >= 4 ? 8 : 16;
+  switch (mode) {
+    case kPlain: return (const void*)k_spmv<G, K, kPlain>;
+    case kCocg: return (const void*)k_spmv<G, K, kCocg>;
+    case kResid: return (const void*)k_spmv<G, K, kResid>;
+    case kResidNR: return (const void*)k_spmv<G, K, kResidNR>;
+    case kSmooth: return (const void*)k_spmv<G, K, kSmooth>;
+    default: return (const void*)k_spmv<G, K, kSmoothDot>;
   }
-#undef ECT_NBE
-#undef ECT_NBEP
 }
-
-// Staged NB kernels (ECT_NB_VARIANT 30/31): function, warps per CTA, nodes per warp.
-struct NbsCfg {
-  const void* fn = nullptr;
-  int nwarp = 0, npw = 0;
-};
 template <int K>
-NbsCfg nbs_cfg(int variant, int mode) {
-#define ECT_NBS(G_, CL_, NW_)                                                              \
-  NbsCfg{mode == kPlain  ? (const void*)k_nbs_spmv<G_, K, kPlain, CL_, NW_>                \
-         : mode == kCocg ? (const void*)k_nbs_spmv<G_, K, kCocg, CL_, NW_>                 \
-                         : (const void*)k_nbs_spmv<G_, K, kResid, CL_, NW_>,               \
-         NW_, 32 / G_}
-  if (variant < 30 || variant > 33) return NbsCfg{};
-  if constexpr (K == 8) {
-    switch (variant) {
-      case 30: return ECT_NBS(4, 4, 8);
-      case 31: return ECT_NBS(8, 4, 16);
-      case 32: return ECT_NBS(8, 8, 16);
-      default: return ECT_NBS(8, 8, 8);
-    }
-  } else if constexpr (K == 4) {
-    switch (variant) {
-      case 30: return ECT_NBS(2, 2, 4);
-      case 31: return ECT_NBS(4, 2, 8);
-      case 32: return ECT_NBS(4, 4, 16);
-      default: return ECT_NBS(8, 4, 16);
-    }
-  } else if constexpr (K == 2) {
-    switch (variant) {
-      case 30: return ECT_NBS(2, 1, 4);
-      case 31: return ECT_NBS(4, 1, 8);
-      case 32: return ECT_NBS(4, 2, 8);
-      default: return ECT_NBS(8, 2, 16);
-    }
-  }
-  return NbsCfg{};
-#undef ECT_NBS
+const void* sell_fn(int mode) {
+  return mode == kPlain  ? (const void*)k_sell_spmv<K, kPlain>
+         : mode == kCocg ? (const void*)k_sell_spmv<K, kCocg>
+                         : (const void*)k_sell_spmv<K, kResid>;
 }
 
-int nbs_cap(ect_matrix* a, int npw) {
-  const int slot = npw == 4 ? 0 : npw == 8 ? 1 : 2;
-  if (a->nbs_cap[slot] < 0) {
-    ect_ctx* ctx = a->ctx;
-    DevBuf<int> cap(1);
-    CK(cudaMemsetAsync(cap.p, 0, sizeof(int), ctx->stream));
-    k_nbs_cap<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(a->nb_blk_ptr, a->n_nodes, npw, cap.p);
-    CK_LAUNCH();
-    int h = 0;
-    CK(cudaMemcpyAsync(&h, cap.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    a->nbs_cap[slot] = (h + 3) & ~3;
-  }
-  return a->nbs_cap[slot];
-}
-
-// dynamic shared memory of a staged launch (0: does not fit, use NB)
-template <int K>
-size_t nbs_bytes(const NbsCfg& c, ect_matrix* a, int mode) {
-  if (!c.fn || !a->has_nb) return 0;
-  const int cap = nbs_cap(a, c.npw);
-  const int cl_nv = mode == kCocg ? 2 * K : mode == kResid ? K : 1;
-  const size_t b = (size_t)c.nwarp * kSlots * nbs_slot_bytes(cap) +
-                   (size_t)c.nwarp * kSlots * sizeof(uint64_t) + 32 * (size_t)std::max(cl_nv, 8) * 8;
-  return b <= 227 * 1024 ? b : 0;
+// Storage used by the SpMV of a matrix: NB-E when built, else SELL, else CSR.
+enum class Store { kNbe, kSell, kCsr };
+inline Store store_of(const ect_matrix* a, int mode) {
+  if (a->has_nb && a->has_nbe) return Store::kNbe;
+  if (a->has_sell && (mode == kPlain || mode == kCocg || mode == kResid)) return Store::kSell;
+  return Store::kCsr;
 }
 
 template <int K>
 struct Dispatch {
   static constexpr int kWidth = K;
-  static constexpr bool kNbOk = K <= 16;
-  static constexpr bool kNbtOk = K <= 4;
-  static bool use_nbt(const ect_matrix* a) {
-    return kNbtOk && a->has_nbt && nbt_smem<K>(a) <= kNbtMaxSmem;
-  }
   static void spmv(ect_ctx* ctx, int mode, int grid, int64_t n, const ect_matrix* a,
                    const double2* x, double2* y, const double2* b, KrylovCtl ctl) {
     cudaStream_t s = ctx->stream;
-    if constexpr (kNbtOk) {
-      if (use_nbt(a)) {
-        const NbtView v = nbt_view(a);
-        const size_t sm = nbt_smem<K>(a);
-        if (mode == kPlain)
-          k_nbt_spmv<K, kPlain><<<grid, kBlock, sm, s>>>(v, x, y, b, ctl);
-        else if (mode == kCocg)
-          k_nbt_spmv<K, kCocg><<<grid, kBlock, sm, s>>>(v, x, y, b, ctl);
-        else
-          k_nbt_spmv<K, kResid><<<grid, kBlock, sm, s>>>(v, x, y, b, ctl);
-        CK_LAUNCH();
-        return;
-      }
-    }
-    if constexpr (kNbOk) {
-      if (a->has_nb) {
+    switch (store_of(a, mode)) {
+      case Store::kNbe: {
         NbView v = nb_view(a);
-        const NbsCfg c = nbs_cfg<K>(ctx->nb_variant, mode);
-        if (const size_t sm = nbs_bytes<K>(c, const_cast<ect_matrix*>(a), mode)) {
-          int cap = nbs_cap(const_cast<ect_matrix*>(a), c.npw);
-          void* args[] = {&v, &cap, &x, &y, &b, &ctl};
-          CK(cudaLaunchKernel(c.fn, dim3(grid), dim3(32 * c.nwarp), args, sm, s));
-          return;
-        }
-        if (a->has_nbe) {
-          v.blk = reinterpret_cast<const double*>(a->nbe_blk.p);
-          v.blk_col = a->nbe_col.p;
-          v.nblk = a->nbe_slots;
-          v.e_off = a->nbe_off.p;
-          void* args[] = {&v, &x, &y, &b, &ctl};
-          CK(cudaLaunchKernel(nbe_fn<K>(ctx->nb_variant, mode), dim3(grid), dim3(kBlock), args, 0,
-                              s));
-          return;
-        }
+        v.blk = reinterpret_cast<const double*>(a->nbe_blk.p);
+        v.blk_col = a->nbe_col.p;
+        v.nblk = a->nbe_slots;
+        v.e_off = a->nbe_off.p;
         void* args[] = {&v, &x, &y, &b, &ctl};
-        CK(cudaLaunchKernel(nb_fn<K>(ctx->nb_variant, mode), dim3(grid), dim3(kBlock), args, 0, s));
+        CK(cudaLaunchKernel(nbe_fn<K>(mode), dim3(grid), dim3(kBlock), args, 0, s));
         return;
       }
+      case Store::kSell: {
+        const int64_t nc = a->sell_chunks;
+        const int* off = a->sell_off.p;
+        const int* perm = a->sell_perm.p;
+        const int* scol = a->sell_col.p;
+        const double2* sval = a->sell_val.p;
+        void* args[] = {(void*)&nc, (void*)&off, (void*)&perm, (void*)&scol, (void*)&sval,
+                        (void*)&x, (void*)&y, (void*)&b, (void*)&ctl};
+        CK(cudaLaunchKernel(sell_fn<K>(mode), dim3(grid), dim3(kBlock), args, 0, s));
+        return;
+      }
+      case Store::kCsr:
+        csr(ctx, mode, grid, n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
+        return;
     }
-    if (a->has_sell) {
-      const int64_t nc = a->sell_chunks;
-      if (mode == kPlain)
-        k_sell_spmv<K, kPlain><<<grid, kBlock, 0, s>>>(nc, a->sell_off.p, a->sell_perm.p,
-                                                        a->sell_col.p, a->sell_val.p, x, y, b, ctl);
-      else if (mode == kCocg)
-        k_sell_spmv<K, kCocg><<<grid, kBlock, 0, s>>>(nc, a->sell_off.p, a->sell_perm.p,
-                                                       a->sell_col.p, a->sell_val.p, x, y, b, ctl);
-      else
-        k_sell_spmv<K, kResid><<<grid, kBlock, 0, s>>>(nc, a->sell_off.p, a->sell_perm.p,
-                                                        a->sell_col.p, a->sell_val.p, x, y, b, ctl);
-      CK_LAUNCH();
-      return;
-    }
-    constexpr int G = K >= 4 ? 8 : 16;
-    if (mode == kPlain)
-      k_spmv<G, K, kPlain><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
-    else if (mode == kCocg)
-      k_spmv<G, K, kCocg><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
-    else
-      k_spmv<G, K, kResid><<<grid, kBlock, 0, s>>>(n, a->row_ptr.p, a->col.p, a->val.p, x, y, b, ctl);
-    CK_LAUNCH();
+  }
+  // plain complex CSR (also the coarse multigrid levels)
+  static void csr(ect_ctx* ctx, int mode, int grid, int64_t n, const int* rp, const int* cl,
+                  const double2* vl, const double2* x, double2* y, const double2* b,
+                  KrylovCtl ctl) {
+    void* args[] = {(void*)&n, (void*)&rp, (void*)&cl, (void*)&vl, (void*)&x, (void*)&y,
+                    (void*)&b, (void*)&ctl};
+    CK(cudaLaunchKernel(csr_fn<K>(mode), dim3(grid), dim3(kBlock), args, 0, ctx->stream));
   }
   static void update(ect_ctx* ctx, int grid, int64_t n, double2* r, const double2* q,
                      const double2* dinv, KrylovCtl ctl) {
@@ -2200,38 +1412,11 @@ struct Dispatch {
     CK_LAUNCH();
   }
   static int spmv_grid(ect_ctx* ctx, int mode, const ect_matrix* a) {
-    if constexpr (kNbtOk) {
-      if (use_nbt(a)) {
-        const void* f = mode == kPlain  ? nbt_fn<K, kPlain>()
-                        : mode == kCocg ? nbt_fn<K, kCocg>()
-                                        : nbt_fn<K, kResid>();
-        const size_t sm = nbt_smem<K>(a);
-        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        return (int)std::min<int64_t>(grid_for(ctx, f, kBlock, sm), a->nbt_tiles);
-      }
+    switch (store_of(a, mode)) {
+      case Store::kNbe: return grid_for(ctx, nbe_fn<K>(mode), kBlock);
+      case Store::kSell: return grid_for(ctx, sell_fn<K>(mode), kBlock);
+      default: return grid_for(ctx, csr_fn<K>(mode), kBlock);
     }
-    if constexpr (kNbOk) {
-      if (a->has_nb) {
-        const NbsCfg c = nbs_cfg<K>(ctx->nb_variant, mode);
-        if (const size_t sm = nbs_bytes<K>(c, const_cast<ect_matrix*>(a), mode)) {
-          CK(cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-          return ctx->num_sms;  // one CTA per SM (the ring fills shared memory)
-        }
-        if (a->has_nbe) return grid_for(ctx, nbe_fn<K>(ctx->nb_variant, mode), kBlock);
-        return grid_for(ctx, nb_fn<K>(ctx->nb_variant, mode), kBlock);
-      }
-    }
-    if (a->has_sell) {
-      const void* f = mode == kPlain  ? (const void*)k_sell_spmv<K, kPlain>
-                      : mode == kCocg ? (const void*)k_sell_spmv<K, kCocg>
-                                      : (const void*)k_sell_spmv<K, kResid>;
-      return grid_for(ctx, f, kBlock);
-    }
-    constexpr int G = K >= 4 ? 8 : 16;
-    const void* f = mode == kPlain  ? (const void*)k_spmv<G, K, kPlain>
-                    : mode == kCocg ? (const void*)k_spmv<G, K, kCocg>
-                                    : (const void*)k_spmv<G, K, kResid>;
-    return grid_for(ctx, f, kBlock);
   }
   static int vec_grid(ect_ctx* ctx) { return grid_for(ctx, (const void*)k_update<K>, kBlock); }
 };
@@ -2324,13 +1509,16 @@ void prof_collect(ect_ctx* ctx) {
       } else {
         ctx->timings.spmv_partial_launches += 1;
       }
-    } else {
+    } else if (P.kinds[i] == 1) {
       if (full) {
         ctx->timings.vec_ms_total += ms;
         ctx->timings.vec_launches += 1;
       } else {
         ctx->timings.vec_partial_launches += 1;
       }
+    } else if (full) {
+      ctx->timings.precond_ms_total += ms;
+      ctx->timings.precond_launches += 1;
     }
   }
   P.used = 0;
@@ -2352,7 +1540,7 @@ void compute_jacobi(ect_matrix* a) {
   int h = 0;
   CK(cudaMemcpyAsync(&h, missing.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  (void)h;  // zero diagonals fall back to identity scaling (reported by the solve if singular)
+  a->n_zero_diag = h;  // a Jacobi solve on such a matrix is a SolverError (cocg_solve)
 }
 
 void build_nb(ect_mesh* m, ect_matrix* a) {
@@ -2382,7 +1570,6 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
   CK(cudaStreamSynchronize(s));
   a->nb_blocks = nblk;
   a->nb_ncpl = ncpl;
-  for (int& c : a->nbs_cap) c = -1;
   a->nb_blk.alloc(6 * (std::max<int64_t>(1, nblk) + 4));  // + staged-copy overrun padding
   a->nb_cpl_idx.alloc(std::max(1, ncpl));
   a->nb_cpl.alloc(4 * (size_t)std::max(1, ncpl));
@@ -2413,7 +1600,7 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
   }
   // ---- NB-E sliced-ELL copy of the blocks (chunks of 32 nodes) -----------------
   a->has_nbe = false;
-  if (ctx->use_nbe) {
+  {
     const int64_t nch = (nn + 31) / 32;
     DevBuf<int> w(nch + 1);
     const int cg = (int)std::min<int64_t>((nch + 255) / 256, (int64_t)ctx->num_sms * 16);
@@ -2438,45 +1625,6 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
     a->nbe_slots = slots;
     a->has_nbe = true;
   }
-  // ---- NB-T tile footprints --------------------------------------------------
-  a->has_nbt = false;
-  if (ctx->no_tiles) return;
-  const int64_t ntiles = (nn + kTileW - 1) / kTileW;
-  DevBuf<int> fcnt(ntiles + 1);
-  CK(cudaMemsetAsync(fcnt.p, 0, fcnt.bytes(), s));
-  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
-  const int tgrid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 8);
-  k_tile_footprint<<<tgrid, 512, 0, s>>>(m->nbr_off.p, m->nbr.p, a->nb_cpl_ptr.p,
-                                        a->nb_cpl_idx.p, nn, ntiles, 0, nullptr, fcnt.p, nullptr,
-                                        nullptr, nullptr, bad.p);
-  CK_LAUNCH();
-  a->nbt_fp_off.alloc(ntiles + 1);
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, fcnt.p, a->nbt_fp_off.p, ntiles + 1, s));
-  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, fcnt.p, a->nbt_fp_off.p,
-                                   ntiles + 1, s));
-  int fmax = 0, ftot = 0;
-  {
-    DevBuf<int> mx(1);
-    CK(cub::DeviceReduce::Max(nullptr, tmp, fcnt.p, mx.p, ntiles, s));
-    CK(cub::DeviceReduce::Max(cub_scratch(ctx, tmp), tmp, fcnt.p, mx.p, ntiles, s));
-    CK(cudaMemcpyAsync(&fmax, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&ftot, a->nbt_fp_off.p + ntiles, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  if (h_bad || fmax <= 0) return;  // too irregular for 16-bit tiles: untiled NB
-  a->nbt_fp_node.alloc(std::max(1, ftot));
-  a->nbt_lcol.alloc(std::max<int64_t>(1, nblk));
-  a->nbt_cpl_lcol.alloc(std::max(1, ncpl));
-  k_tile_footprint<<<tgrid, 512, 0, s>>>(m->nbr_off.p, m->nbr.p, a->nb_cpl_ptr.p,
-                                        a->nb_cpl_idx.p, nn, ntiles, 1, a->nbt_fp_off.p, fcnt.p,
-                                        a->nbt_fp_node.p, a->nbt_lcol.p, a->nbt_cpl_lcol.p, bad.p);
-  CK_LAUNCH();
-  note_launch(ctx, 2);
-  CK(cudaStreamSynchronize(s));
-  a->nbt_tiles = ntiles;
-  a->nbt_fmax = fmax;
-  a->has_nbt = true;
 }
 
 void build_sell(ect_matrix* a, int sigma) {
@@ -2860,8 +2008,10 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       if (t.status == kBreakdown) {
         // a (near-)breakdown of the Lanczos recurrences: restart from the true
         // residual (new shadow vector); an error only when it recurs at once
-        if (restart_round >= 32 || t.iters >= opt.max_iter || t.iters == last_break[c])
-          fail(ECT_ERR_SOLVER, "BiCGStab breakdown on right-hand side " + std::to_string(c));
+        if (restart_round >= 32 || t.iters >= opt.max_iter || t.iters == last_break[c]) {
+          out->breakdown[c] = 1;  // reported per column; ect_solve raises SolverError
+          continue;
+        }
         last_break[c] = t.iters;
         restart_mask |= 1u << c;
         continue;
@@ -2898,14 +2048,209 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
 
 }  // namespace
 
+// ---- aggregation-multigrid cycle (setup in amg.cu) ----------------------------
+// M r for the preconditioned COCG: per level l with right-hand side b_l
+//   x = omega D^-1 b                 (k_vscale)
+//   t = b - A x                      (SpMV, kResidNR)
+//   b_{l+1} = P^T t                  (k_restrict: sum over the aggregate's dofs)
+//   e = cycle(l+1, b_{l+1})          (W-cycle: a second visit on b_{l+1} - A e)
+//   x += oc P e                      (k_prolong)
+//   y = x + omega D^-1 (b - A x)     (SpMV, kSmooth; on level 0 kSmoothDot also
+//                                     forms r^T z -> rho, beta)
+// and a dense inverse on the coarsest level. Symmetric pre/post smoothing and
+// the plain transpose keep M complex symmetric (M = M^T), as COCG requires.
+namespace {
+
+__device__ __forceinline__ bool idle(const int* n_active) { return *n_active == 0; }
+
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_vscale(int64_t n, const double2* __restrict__ b, const double2* __restrict__ dinv, double omega,
+         double2* __restrict__ x, const int* n_active) {
+  if (idle(n_active)) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 d = dinv[e / K];
+    x[e] = cmul(make_double2(omega * d.x, omega * d.y), b[e]);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_restrict(int64_t nc, const int* __restrict__ r_ptr, const int* __restrict__ r_idx,
+           const double2* __restrict__ t, double2* __restrict__ bc, const int* n_active) {
+  if (idle(n_active)) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nc * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / K, k = e - c * K;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int p = r_ptr[c]; p < r_ptr[c + 1]; ++p) acc = cadd(acc, t[(int64_t)r_idx[p] * K + k]);
+    bc[e] = acc;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_prolong(int64_t n, const int* __restrict__ cmap, double oc, const double2* __restrict__ ec,
+          double2* __restrict__ x, const int* n_active) {
+  if (idle(n_active)) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / K;
+    const int c = cmap[i];
+    if (c < 0) continue;
+    const double2 v = ec[(int64_t)c * K + (e - i * K)];
+    x[e] = cadd(x[e], make_double2(oc * v.x, oc * v.y));
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_axpy1(int64_t n, double2* __restrict__ y, const double2* __restrict__ x, const int* n_active) {
+  if (idle(n_active)) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
+       e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = cadd(y[e], x[e]);
+}
+
+// x = Minv b on the coarsest level: warp per row, fixed-order lane/shuffle sums
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_dense(int64_t n, const double2* __restrict__ minv, const double2* __restrict__ b,
+        double2* __restrict__ x, const int* n_active) {
+  if (idle(n_active)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += n_warps) {
+    double2 acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
+    for (int64_t j = lane; j < n; j += 32) {
+      const double2 m = minv[i * n + j];
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = cadd(acc[k], cmul(m, b[j * K + k]));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, o);
+        acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, o);
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < K; ++k) x[i * K + k] = acc[k];
+  }
+}
+
+template <int K>
+struct Cycle {
+  using DK = Dispatch<K>;
+  ect_ctx* ctx;
+  ect_matrix* a;
+  Amg& H;
+  int grid0[6] = {};                  // level-0 SpMV grids per mode
+  std::vector<std::array<int, 6>> gl;  // levels >= 1
+  int gvec(int64_t work) const {
+    const int64_t b = (work + kBlock - 1) / kBlock;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx->num_sms * 8));
+  }
+  Cycle(ect_ctx* c, ect_matrix* m, Amg& h) : ctx(c), a(m), H(h) {
+    for (int mode : {kResidNR, kSmooth, kSmoothDot}) grid0[mode] = DK::spmv_grid(ctx, mode, a);
+    gl.resize(H.lv.size());
+    constexpr int G = K >= 4 ? 8 : 16;
+    for (size_t l = 1; l < H.lv.size(); ++l)
+      for (int mode : {kResidNR, kSmooth}) {
+        const int64_t need = (H.lv[l].n * G + kBlock - 1) / kBlock;
+        gl[l][mode] = (int)std::max<int64_t>(
+            1, std::min<int64_t>(need, grid_for(ctx, csr_fn<K>(mode), kBlock)));
+      }
+    // work vectors for this batch width
+    if (H.kcap < K) {
+      for (size_t l = 0; l + 1 < H.lv.size(); ++l) {
+        AmgLevel& L = H.lv[l];
+        L.xt.alloc((size_t)L.n * K);
+        if (l > 0) L.t.alloc((size_t)L.n * K);
+      }
+      for (size_t l = 1; l < H.lv.size(); ++l) {
+        AmgLevel& L = H.lv[l];
+        for (auto* v : {&L.b, &L.out, &L.b2, &L.out2}) v->alloc((size_t)L.n * K);
+      }
+      H.kcap = K;
+    }
+  }
+  int max_grid() const { return std::max({grid0[kResidNR], grid0[kSmooth], grid0[kSmoothDot]}); }
+  void spmv(size_t l, int mode, const double2* x, double2* y, const double2* b, KrylovCtl c) {
+    if (l == 0) {
+      c.dinv = a->dinv.p;
+      DK::spmv(ctx, mode, grid0[mode], a->n, a, x, y, b, c);
+    } else {
+      AmgLevel& L = H.lv[l];
+      c.dinv = L.dinv.p;
+      DK::csr(ctx, mode, gl[l][mode], L.n, L.row_ptr.p, L.col.p, L.val.p, x, y, b, c);
+    }
+  }
+  // out = M_l b; t0 = a free level-0 vector (COCG's q)
+  void run(size_t l, const double2* b, double2* out, double2* t0, KrylovCtl c, bool dot) {
+    cudaStream_t s = ctx->stream;
+    AmgLevel& L = H.lv[l];
+    const int64_t n = L.n;
+    const int* na = c.n_active;
+    if (l + 1 == H.lv.size()) {
+      const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n * 32 + kBlock - 1) / kBlock,
+                                                                 (int64_t)ctx->num_sms * 8));
+      k_dense<K><<<g, kBlock, 0, s>>>(n, H.minv.p, b, out, na);
+      CK_LAUNCH();
+      note_launch(ctx, 1);
+      return;
+    }
+    c.omega = H.omega;
+    const double2* dinv = l == 0 ? a->dinv.p : L.dinv.p;
+    double2* xt = L.xt.p;
+    double2* t = l == 0 ? t0 : L.t.p;
+    k_vscale<K><<<gvec(n * K), kBlock, 0, s>>>(n, b, dinv, H.omega, xt, na);
+    CK_LAUNCH();
+    spmv(l, kResidNR, xt, t, b, c);
+    AmgLevel& C = H.lv[l + 1];
+    k_restrict<K><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, L.r_ptr.p, L.r_idx.p, t, C.b.p, na);
+    CK_LAUNCH();
+    run(l + 1, C.b.p, C.out.p, t0, c, false);
+    if (H.wcycle && l + 2 < H.lv.size()) {
+      spmv(l + 1, kResidNR, C.out.p, C.b2.p, C.b.p, c);
+      run(l + 1, C.b2.p, C.out2.p, t0, c, false);
+      k_axpy1<K><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, C.out.p, C.out2.p, na);
+      CK_LAUNCH();
+      note_launch(ctx, 2);
+    }
+    k_prolong<K><<<gvec(n * K), kBlock, 0, s>>>(n, L.cmap.p, H.oc, C.out.p, xt, na);
+    CK_LAUNCH();
+    spmv(l, dot ? kSmoothDot : kSmooth, xt, out, b, c);
+    note_launch(ctx, 5);
+  }
+};
+
+}  // namespace
+
+void throw_on_breakdown(const SolveOut& out) {
+  for (size_t c = 0; c < out.breakdown.size(); ++c)
+    if (out.breakdown[c])
+      fail(ECT_ERR_SOLVER, "Krylov breakdown (p^T A p or r^T z vanished) on right-hand side " +
+                               std::to_string(c));
+}
+
 void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k,
                 const ect_iter_options& opt, SolveOut* out) {
   if (!(opt.tol > 0.0)) fail(ECT_ERR_SOLVER, "solve_iterative: tolerance must be positive");
   if (k < 1 || k > 16) fail(ECT_ERR_SOLVER, "solve: n_rhs must be in 1..16");
   if (!a->symmetric) {  // impedance surface terms: A != A^T
+    if (a->n_zero_diag > 0)
+      fail(ECT_ERR_SOLVER, "Jacobi preconditioner: " + std::to_string(a->n_zero_diag) +
+                               " rows have a zero diagonal");
     out->iters.assign(k, 0);
     out->residual.assign(k, 0.0);
     out->converged.assign(k, 0);
+    out->breakdown.assign(k, 0);
     int kb = 1;
     while (kb < k) kb <<= 1;
     with_k(kb, [&](auto D) {
@@ -2923,17 +2268,29 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
   out->iters.assign(k, 0);
   out->residual.assign(k, 0.0);
   out->converged.assign(k, 0);
+  out->breakdown.assign(k, 0);
+
+  // preconditioner: multigrid (built once per matrix) or point Jacobi
+  const bool ext = a->precond == ECT_PRECOND_AMG;
+  if (ext && !a->amg) amg_setup(a);
+  if (!ext && a->n_zero_diag > 0)
+    fail(ECT_ERR_SOLVER, "Jacobi preconditioner: " + std::to_string(a->n_zero_diag) +
+                             " rows have a zero diagonal");
 
   with_k(kk, [&](auto D) {
     using DK = decltype(D);
+    constexpr int KW = DK::kWidth;
     const int grid_s = DK::spmv_grid(ctx, kCocg, a);
     const int grid_r = DK::spmv_grid(ctx, kResid, a);
     const int grid_v = DK::vec_grid(ctx);
-    const int grid_max = std::max(std::max(grid_s, grid_r), grid_v);
+    std::unique_ptr<Cycle<KW>> cyc;
+    if (ext) cyc = std::make_unique<Cycle<KW>>(ctx, a, *a->amg);
+    const int grid_max = std::max({grid_s, grid_r, grid_v, cyc ? cyc->max_grid() : 0});
     const size_t vec = (size_t)n * kk;
     // workspace cached on the context (a sweep solves thousands of times)
     auto& W = ctx->ws;
     for (auto* v : {&W.bb, &W.xx, &W.r, &W.p, &W.q}) v->ensure(vec);
+    if (ext) W.z.ensure(vec);
     W.st.ensure(kk);
     W.n_active.ensure(1);
     W.counter.ensure(1);
@@ -2957,8 +2314,22 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
     KrylovCtl ctl{st.p, n_active.p, counter.p, partial.p, opt.tol, opt.max_iter,
                   nullptr, 0, n, n, n};
     const unsigned all = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
-    DK::start(ctx, grid_v, n, bb.p, xx.p, r.p, p.p, a->dinv.p, all, 1, ctl);
-    note_launch(ctx, 1);
+    // (re)start: norms (+ p = D^-1 r, rho with Jacobi); multigrid then sets
+    // p = M r and rho = r^T M r
+    auto start = [&](unsigned mask, int fresh) {
+      if (ext) {
+        k_start<KW, true><<<grid_v, kBlock, 0, s>>>(n, bb.p, xx.p, r.p, p.p, nullptr, mask, fresh,
+                                                     ctl);
+        CK_LAUNCH();
+        KrylovCtl c = ctl;
+        c.rho_start = 1;
+        cyc->run(0, r.p, p.p, q.p, c, true);
+      } else {
+        DK::start(ctx, grid_v, n, bb.p, xx.p, r.p, p.p, a->dinv.p, mask, fresh, ctl);
+      }
+      note_launch(ctx, 1);
+    };
+    start(all, 1);
 
     std::vector<RhsState> hs(kk);
     int* flag = ctx->pinned_flag;
@@ -2979,9 +2350,22 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
           ev2[0] = ev2[1] = nullptr;
           // same sampled iterations as the SpMV, same active-column snapshot
           if (ev[0]) prof_begin(ctx, ev2, 1, false, nullptr, k, prof_snap_of(ctx, ev[0]));
-          DK::update(ctx, grid_v, n, r.p, q.p, a->dinv.p, ctl);
-          DK::pupdate(ctx, grid_v, n, xx.p, r.p, p.p, a->dinv.p, ctl);
-          prof_end(ctx, ev2);
+          if (ext) {
+            k_update<KW, true><<<grid_v, kBlock, 0, s>>>(n, r.p, q.p, nullptr, ctl);
+            CK_LAUNCH();
+            prof_end(ctx, ev2);
+            cudaEvent_t ev3[2];
+            ev3[0] = ev3[1] = nullptr;
+            if (ev[0]) prof_begin(ctx, ev3, 2, false, nullptr, k, prof_snap_of(ctx, ev[0]));
+            cyc->run(0, r.p, W.z.p, q.p, ctl, true);  // z = M r, rho, beta
+            prof_end(ctx, ev3);
+            k_pupdate<KW, true><<<grid_v, kBlock, 0, s>>>(n, xx.p, r.p, p.p, nullptr, ctl, W.z.p);
+            CK_LAUNCH();
+          } else {
+            DK::update(ctx, grid_v, n, r.p, q.p, a->dinv.p, ctl);
+            DK::pupdate(ctx, grid_v, n, xx.p, r.p, p.p, a->dinv.p, ctl);
+            prof_end(ctx, ev2);
+          }
           note_launch(ctx, 3);
         }
         launched += chunk;
@@ -3020,10 +2404,7 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       unsigned restart_mask = 0;
       for (int c = 0; c < k; ++c) {
         RhsState& t = hs[c];
-        if (t.status == kBreakdown) {
-          fail(ECT_ERR_SOLVER, "COCG breakdown (p^T A p or r^T z vanished) on right-hand side " +
-                                   std::to_string(c));
-        }
+        if (t.status == kBreakdown) continue;  // reported per column (SolveOut::breakdown)
         const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
         if (t.status == kConverged && rel > opt.tol && t.iters < opt.max_iter &&
             restart_round < 8) {
@@ -3036,8 +2417,7 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
         if ((restart_mask >> c) & 1u)
           CK(cudaMemcpy2DAsync(r.p + c, kk * sizeof(double2), q.p + c, kk * sizeof(double2),
                                sizeof(double2), n, cudaMemcpyDeviceToDevice, s));
-      DK::start(ctx, grid_v, n, bb.p, xx.p, r.p, p.p, a->dinv.p, restart_mask, 0, ctl);
-      note_launch(ctx, 1);
+      start(restart_mask, 0);
       // keep the other columns frozen
       CK(cudaStreamSynchronize(s));
     }
@@ -3047,6 +2427,7 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       const double rel = t.bnorm > 0.0 ? t.rnorm / t.bnorm : 0.0;
       out->residual[c] = rel;
       out->converged[c] = (t.status == kZeroRhs) || (t.status == kConverged && rel <= opt.tol);
+      out->breakdown[c] = t.status == kBreakdown;
     }
     if (kk == k) {
       CK(cudaMemcpyAsync(x, xx.p, vec * sizeof(double2), cudaMemcpyDeviceToDevice, s));
@@ -3115,8 +2496,9 @@ NbView part_view(const ect_part* P) {
 }
 
 template <int K>
-const void* part_fn(const ect_part* P, int variant, int mode) {
-  return P->has_nbe ? nbe_fn<K>(variant, mode) : nb_fn<K>(variant, mode);
+const void* part_fn(const ect_part* P, int mode) {
+  (void)P;
+  return nbe_fn<K>(mode);
 }
 
 }  // namespace
@@ -3234,7 +2616,7 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
     P->peers.push_back(std::move(d));
   }
   // NB-E copy of the part's blocks (same layout and kernels as a whole matrix)
-  if (ctx->use_nbe) {
+  {
     const int64_t nch = (L + 31) / 32;
     DevBuf<int> w(nch + 1);
     const int cg = (int)std::min<int64_t>((nch + 255) / 256, (int64_t)ctx->num_sms * 16);
@@ -3285,7 +2667,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
   for (int r = 0; r < R; ++r)
     if (parts[r]->ctx != ctx) fail(ECT_ERR_SOLVER, "dist_solve: in-process parts must share a context");
   if (comm && R != 1) fail(ECT_ERR_SOLVER, "dist_solve: with a communicator each process owns one part");
-  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], ctx->nb_variant, kCocg), kBlock);
+  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], kCocg), kBlock);
   const int grid_v = DK::vec_grid(ctx);
   const int grid_max = std::max(grid_s, grid_v);
   const int64_t na_g = parts[0]->na_global;
@@ -3387,7 +2769,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
     KrylovCtl c = S[r].ctl;
     c.red_add = add ? 1 : 0;
     void* args[] = {&v, &xp, &yp, &bp, &c};
-    CK(cudaLaunchKernel(part_fn<K>(parts[r], ctx->nb_variant, mode), dim3(grid_s), dim3(kBlock),
+    CK(cudaLaunchKernel(part_fn<K>(parts[r], mode), dim3(grid_s), dim3(kBlock),
                         args, 0, s));
   };
   auto spmv = [&](int mode, DevBuf<double2> PartState<K>::*xin, DevBuf<double2> PartState<K>::*yout,

@@ -184,7 +184,167 @@ __global__ void k_csr_to_csc(const int* __restrict__ row_ptr, const int* __restr
   }
 }
 
+// Compressed-major -> the other major (CSC -> CSR or CSR -> CSC): expand
+// the major index of every entry; a stable radix sort by minor index then
+// yields the transposed order (ties keep the input order = ascending major).
+__global__ void k_expand_major(const int* __restrict__ ptr, int64_t n, int* __restrict__ major) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = warp; j < n; j += n_warps)
+    for (int p = ptr[j] + lane; p < ptr[j + 1]; p += 32) major[p] = (int)j;
+}
+
+__global__ void k_iota(int* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int)i;
+}
+
+__global__ void k_gather_entries(const int* __restrict__ perm, const int* __restrict__ major,
+                                 const double2* __restrict__ val, int64_t nnz,
+                                 int* __restrict__ out_idx, double2* __restrict__ out_val) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int p = perm[q];
+    out_idx[q] = major[p];
+    out_val[q] = val[p];
+  }
+}
+
+__global__ void k_count_minor(const int* __restrict__ minor, int64_t nnz, int* __restrict__ cnt) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + minor[q], 1);
+}
+
+__global__ void k_check_index(const int* __restrict__ ptr, const int* __restrict__ idx, int64_t n,
+                              int64_t nnz, int* bad) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x)
+    if (idx[q] < 0 || idx[q] >= n) atomicOr(bad, 1);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    if (ptr[j + 1] < ptr[j]) atomicOr(bad, 2);
+}
+
+__device__ __forceinline__ double cabs2(double2 v) { return sqrt(v.x * v.x + v.y * v.y); }
+
+// Symmetry probe: the transposed arrays (CSR of A^T) against the CSR of A.
+// Pattern mismatch -> flag 1; value mismatch beyond 1e-12 sqrt(|a_ii a_jj|)
+// (SURVEY D10's scale; A is symmetric only up to rounding) -> flag 2.
+__global__ void k_symmetry(const int* __restrict__ rp, const int* __restrict__ col,
+                           const double2* __restrict__ val, const int* __restrict__ trp,
+                           const int* __restrict__ tcol, const double2* __restrict__ tval,
+                           const double* __restrict__ dabs, int64_t n, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += n_warps) {
+    if (rp[i] != trp[i] || rp[i + 1] != trp[i + 1]) {
+      if (lane == 0) atomicOr(flag, 1);
+      continue;
+    }
+    for (int p = rp[i] + lane; p < rp[i + 1]; p += 32) {
+      const int j = col[p];
+      if (tcol[p] != j) {
+        atomicOr(flag, 1);
+        continue;
+      }
+      const double2 a = val[p], b = tval[p];
+      const double d = hypot(a.x - b.x, a.y - b.y);
+      const double scale = sqrt(dabs[i] * dabs[j]);
+      if (d > 1e-12 * scale && d > 1e-14 * fmax(cabs2(a), cabs2(b))) atomicOr(flag, 2);
+    }
+  }
+}
+
+__global__ void k_diag_abs(const int* __restrict__ rp, const int* __restrict__ col,
+                           const double2* __restrict__ val, int64_t n, double* dabs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double d = 0.0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p)
+      if (col[p] == (int)i) d = cabs2(val[p]);
+    dabs[i] = d;
+  }
+}
+
+// Transpose (ptr, idx, val) of an n x n compressed matrix into (tptr, tidx, tval).
+void transpose_compressed(ect_ctx* ctx, int64_t n, int64_t nnz, const int* ptr, const int* idx,
+                          const double2* val, int* tptr, int* tidx, double2* tval) {
+  cudaStream_t s = ctx->stream;
+  DevBuf<int> major(nnz), perm_in(nnz), perm(nnz), keys_out(nnz), cnt(n + 1);
+  k_expand_major<<<blocks_for(ctx, 32 * n), 256, 0, s>>>(ptr, n, major.p);
+  CK_LAUNCH();
+  k_iota<<<blocks_for(ctx, nnz), 256, 0, s>>>(perm_in.p, nnz);
+  CK_LAUNCH();
+  int bits = 1;
+  while (bits < 31 && (1ll << bits) < n) ++bits;
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, idx, keys_out.p, perm_in.p, perm.p, (int)nnz,
+                                     0, bits, s));
+  CK(cub::DeviceRadixSort::SortPairs(cub_scratch(ctx, tmp), tmp, idx, keys_out.p, perm_in.p,
+                                     perm.p, (int)nnz, 0, bits, s));
+  k_gather_entries<<<blocks_for(ctx, nnz), 256, 0, s>>>(perm.p, major.p, val, nnz, tidx, tval);
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), s));
+  k_count_minor<<<blocks_for(ctx, nnz), 256, 0, s>>>(idx, nnz, cnt.p);
+  CK_LAUNCH();
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.p, tptr, n + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, cnt.p, tptr, n + 1, s));
+  note_launch(ctx, 6);
+  CK(cudaStreamSynchronize(s));
+}
+
 }  // namespace
+
+void matrix_from_compressed(ect_ctx* ctx, int64_t n, int64_t nnz, const int* ptr, const int* idx,
+                            const double2* val, bool csc, ect_matrix* a) {
+  cudaStream_t s = ctx->stream;
+  {
+    DevBuf<int> bad(1);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    k_check_index<<<blocks_for(ctx, std::max(n, nnz)), 256, 0, s>>>(ptr, idx, n, nnz, bad.p);
+    CK_LAUNCH();
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h) fail(ECT_ERR_SOLVER, "matrix: index out of range or decreasing pointer array");
+  }
+  a->n = n;
+  a->nnz = nnz;
+  a->row_ptr.alloc(n + 1);
+  a->col.alloc(nnz);
+  a->val.alloc(nnz);
+  DevBuf<int> tp(n + 1), ti(nnz);
+  DevBuf<double2> tv(nnz);
+  transpose_compressed(ctx, n, nnz, ptr, idx, val, tp.p, ti.p, tv.p);
+  // csc: the transpose IS the CSR of A; csr: the input is, the transpose is A^T
+  const int* rp = csc ? tp.p : ptr;
+  const int* cl = csc ? ti.p : idx;
+  const double2* vl = csc ? tv.p : val;
+  const int* trp = csc ? ptr : tp.p;
+  const int* tcl = csc ? idx : ti.p;
+  const double2* tvl = csc ? val : tv.p;
+  DevBuf<double> dabs(n);
+  DevBuf<int> flag(1);
+  CK(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  k_diag_abs<<<blocks_for(ctx, n), 256, 0, s>>>(rp, cl, vl, n, dabs.p);
+  CK_LAUNCH();
+  k_symmetry<<<blocks_for(ctx, 32 * n), 256, 0, s>>>(rp, cl, vl, trp, tcl, tvl, dabs.p, n, flag.p);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(a->row_ptr.p, rp, (n + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(a->col.p, cl, nnz * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(a->val.p, vl, nnz * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  note_launch(ctx, 3);
+  a->symmetric = h == 0;
+  a->assembled = true;
+  a->precond = ctx->precond;
+}
 
 void export_csc_values(ect_matrix* a, double2* out) {
   ect_ctx* ctx = a->ctx;
@@ -264,6 +424,8 @@ void build_pattern(ect_mesh* m, ect_matrix* a) {
   a->n_nodes = nn;
   a->n_cond = m->n_cond;
   a->from_mesh = true;
+  a->mesh = m;
+  a->precond = ctx->precond;
   a->row_ptr.alloc(N + 1);
   a->col.alloc(std::max<long long>(1, nnz));
   a->val.alloc(std::max<long long>(1, nnz));

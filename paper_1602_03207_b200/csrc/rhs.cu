@@ -67,6 +67,43 @@ __global__ void k_support(const int4* __restrict__ tets, const uint8_t* __restri
   if (local) atomicAdd(count, local);
 }
 
+// assemble_rhs(mesh, support_tets, ...) (assembly.cpp:335-349): flag the
+// support nodes of a caller-supplied tet list (or of every tet of a region
+// when list == nullptr), report the first conductor tet like the reference.
+__global__ void k_support_list(const int4* __restrict__ tets, const uint8_t* __restrict__ region,
+                               const int* __restrict__ list, int64_t n_list, int tag,
+                               int64_t n_tets, uint8_t* node_flag, int* count, int* conductor_hit,
+                               int* bad_index) {
+  int local = 0;
+  const int64_t n = list ? n_list : n_tets;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = list ? (int64_t)list[q] : q;
+    if (t < 0 || t >= n_tets) {
+      atomicMin(bad_index, (int)q);
+      continue;
+    }
+    if (!list && region[t] != tag) continue;
+    ++local;
+    if (is_conductor(region[t])) atomicMin(conductor_hit, (int)t);
+    const int4 k = tets[t];
+    node_flag[k.x] = 1;
+    node_flag[k.y] = 1;
+    node_flag[k.z] = 1;
+    node_flag[k.w] = 1;
+  }
+  if (local) atomicAdd(count, local);
+}
+
+// apply_pins_to_rhs (assembly.cpp:329-333): pinned entries = penalty * 0.
+__global__ void k_pin_rhs(const uint8_t* __restrict__ pinned, int64_t na, int stride,
+                          double2* rhs) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < na * stride;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (pinned[e / stride]) rhs[e] = make_double2(0.0, 0.0);
+  }
+}
+
 __global__ void k_nodal_current(const double* __restrict__ xyz, const uint8_t* __restrict__ flag,
                                 int64_t n_nodes, double amplitude, double* j) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
@@ -119,7 +156,7 @@ __global__ void k_rhs_gather(const int4* __restrict__ tets, const double* __rest
     if (!any) continue;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double v = pinned[3 * i + c] ? 0.0 : out[c];
+      const double v = (pinned && pinned[3 * i + c]) ? 0.0 : out[c];
       rhs[(3 * i + c) * (int64_t)stride + column] = make_double2(v, 0.0);
     }
   }
@@ -278,6 +315,53 @@ void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* wh
     note_launch(ctx, 3);
   }
   CK(cudaStreamSynchronize(s));
+}
+
+void build_rhs_support(ect_mesh* m, const int* support, int64_t n_support, int region_tag,
+                       double amplitude, double2* rhs) {
+  ect_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  const int64_t nn = m->n_nodes, N = 3 * nn + m->n_cond;
+  CK(cudaMemsetAsync(rhs, 0, (size_t)N * sizeof(double2), s));
+  DevBuf<uint8_t> flag(nn);
+  DevBuf<double> j(3 * nn);
+  DevBuf<int> stat(3);
+  CK(cudaMemsetAsync(flag.p, 0, flag.bytes(), s));
+  int init[3] = {0, 0x7fffffff, 0x7fffffff};
+  CK(cudaMemcpyAsync(stat.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  const int64_t n = support ? n_support : m->n_tets;
+  if (n > 0) {
+    k_support_list<<<blocks_for(ctx, n), 256, 0, s>>>(m->tets.p, m->region.p, support, n_support,
+                                                      region_tag, m->n_tets, flag.p, stat.p,
+                                                      stat.p + 1, stat.p + 2);
+    CK_LAUNCH();
+  }
+  int h[3];
+  CK(cudaMemcpyAsync(h, stat.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h[2] != 0x7fffffff) fail(ECT_ERR_MESH, "coil support: tet index out of range");
+  if (h[0] == 0) fail(ECT_ERR_MESH, "coil support is empty");
+  if (h[1] != 0x7fffffff) {
+    fail(ECT_ERR_MESH, "coil support intersects a conductor region (tet " + std::to_string(h[1]) +
+                           "); the source must be divergence-free in the insulator");
+  }
+  k_nodal_current<<<blocks_for(ctx, nn), 256, 0, s>>>(m->xyz.p, flag.p, nn, amplitude, j.p);
+  CK_LAUNCH();
+  // assemble_rhs itself does not pin (position_rhs applies the pins afterwards)
+  k_rhs_gather<<<blocks_for(ctx, nn), 256, 0, s>>>(m->tets.p, m->xyz.p, m->inc_off.p, m->inc.p,
+                                                  flag.p, j.p, nullptr, nn, 1, 0, rhs);
+  CK_LAUNCH();
+  note_launch(ctx, 3);
+  CK(cudaStreamSynchronize(s));
+}
+
+void apply_pins_rhs(ect_mesh* m, double2* rhs, int n_rhs) {
+  ect_ctx* ctx = m->ctx;
+  const int64_t na = 3 * m->n_nodes;
+  k_pin_rhs<<<blocks_for(ctx, na * n_rhs), 256, 0, ctx->stream>>>(m->pinned.p, na, n_rhs, rhs);
+  CK_LAUNCH();
+  note_launch(ctx, 1);
+  CK(cudaStreamSynchronize(ctx->stream));
 }
 
 void delta_impedance(ect_mesh* m, const ect_materials& pm, const ect_materials& rm,

@@ -45,6 +45,8 @@ class CudaError(EctError):
     code = 6
 
 
+PRECOND = {"jacobi": 0, "amg": 1}
+
 _ERRORS = {2: ConfigError, 3: MeshError, 4: SolverError, 5: IoError, 6: CudaError}
 
 
@@ -56,10 +58,18 @@ class Materials(C.Structure):
 
 
 class Physics(C.Structure):
+    """ect_physics == RunConfig [materials] (config.hpp:25-39); NaN = unset optional."""
     _fields_ = [("frequency", D), ("sigma_tube", D), ("mu_r_tube", D), ("sigma_defect", D),
                 ("mu_r_defect", D), ("sigma_eps_ratio", D), ("delta_gauge", D),
                 ("bc_penalty", D), ("mu_tilde_harmonic", I32), ("mu_tilde_fixed", D),
-                ("sigma_tsp", D), ("mu_r_tsp", D), ("ibc_tsp", I32)]
+                ("sigma_tsp", D), ("mu_r_tsp", D), ("ibc_tsp", I32), ("l22_sigma_eps", I32)]
+
+    @classmethod
+    def defaults(cls) -> "Physics":
+        """ect_physics_init: RunConfig's defaults."""
+        ph = cls()
+        lib().ect_physics_init(C.byref(ph))
+        return ph
 
 
 class Coil(C.Structure):
@@ -83,7 +93,8 @@ class Timings(C.Structure):
     _fields_ = [("pattern_ms", D), ("assemble_ms", D), ("rhs_ms", D), ("solve_ms", D),
                 ("spmv_ms_total", D), ("spmv_launches", I64), ("kernel_launches", I64),
                 ("vec_ms_total", D), ("vec_launches", I64),
-                ("spmv_partial_launches", I64), ("vec_partial_launches", I64)]
+                ("spmv_partial_launches", I64), ("vec_partial_launches", I64),
+                ("precond_ms_total", D), ("precond_launches", I64)]
 
 
 _lib = None
@@ -115,11 +126,41 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def _cvec(a, count, name, writable=False):
+    """Validate a complex128 buffer of `count` elements, C-contiguous (numpy or
+    torch, host or device); numpy inputs that are not are converted (inputs
+    only). Buffers handed to the library as raw pointers must match exactly."""
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.dtype != torch.complex128 or not a.is_contiguous() or a.numel() != count:
+            raise ConfigError(f"{name}: need a contiguous complex128 tensor of {count} elements")
+        return a
+    if writable:
+        if (not isinstance(a, np.ndarray) or a.dtype != np.complex128
+                or not a.flags.c_contiguous or a.size != count or not a.flags.writeable):
+            raise ConfigError(f"{name}: need a writable C-contiguous complex128 array of {count} elements")
+        return a
+    a = np.ascontiguousarray(a, np.complex128)
+    if a.size != count:
+        raise ConfigError(f"{name}: expected {count} complex values, got {a.size}")
+    return a
+
+
 def physics_struct(ph) -> Physics:
-    return Physics(ph.frequency, ph.sigma_tube, ph.mu_r_tube, ph.sigma_defect, ph.mu_r_defect,
-                   ph.sigma_eps_ratio, ph.delta_gauge, ph.bc_penalty, int(ph.mu_tilde_harmonic),
-                   ph.mu_tilde_fixed, ph.sigma_tsp, ph.mu_r_tsp,
-                   int(getattr(ph, "ibc_tsp", False)))
+    """workloads.Physics -> ect_physics, starting from ect_physics_init's defaults.
+    A negative / None optional (sigma_defect, mu_r_defect, sigma_tsp, mu_r_tsp)
+    keeps the default (NaN = unset for the std::optional defect keys)."""
+    if isinstance(ph, Physics):
+        return ph
+    out = Physics.defaults()
+    for f, _ in Physics._fields_:
+        if not hasattr(ph, f):
+            continue
+        v = getattr(ph, f)
+        if f in ("sigma_defect", "mu_r_defect", "sigma_tsp", "mu_r_tsp") and (v is None or v < 0):
+            continue
+        setattr(out, f, int(v) if f in ("mu_tilde_harmonic", "ibc_tsp", "l22_sigma_eps") else v)
+    return out
 
 
 class Context:
@@ -152,9 +193,14 @@ class Context:
         _check(lib().ect_ctx_synchronize(self.h))
 
     def set_format(self, fmt: str):
-        """SpMV storage of matrices assembled afterwards: 'nb' (default),
-        'nb_tiled' (shared-memory x tiles) or 'csr'."""
-        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1, "nb_tiled": 2, "sell": 3}[fmt])))
+        """SpMV storage of matrices assembled afterwards: 'nb' (default,
+        sliced-ELL node blocks), 'sell' (SELL-32-sigma) or 'csr'."""
+        _check(lib().ect_ctx_set_format(self.h, C.c_int({"nb": 0, "csr": 1, "sell": 3}[fmt])))
+
+    def set_preconditioner(self, name: str):
+        """Default preconditioner of matrices created afterwards: 'amg'
+        (aggregation multigrid, the default) or 'jacobi'."""
+        _check(lib().ect_ctx_set_preconditioner(self.h, I32(PRECOND[name])))
 
     def mark(self, slot: int):
         """Record event `slot` on the context stream (device-side timing)."""
@@ -213,12 +259,41 @@ class Mesh:
         z = np.ascontiguousarray(np.atleast_1d(z), np.float64)
         which = np.ascontiguousarray(np.atleast_1d(which), np.int32)
         k = z.shape[0]
+        if which.shape[0] != k:
+            raise ConfigError(f"rhs: {k} probe positions but {which.shape[0]} coil indices")
         if out is None:
             out = np.empty((self.n_dofs, k), np.complex128)
+        _cvec(out, self.n_dofs * k, "out", writable=True)
         cs = Coil(*coil)
         _check(lib().ect_rhs_coil(self.ctx.h, self.h, C.byref(cs), _ptr(z), _ptr(which), I32(k),
                                   D(amplitude), _ptr(out)))
         return out
+
+    def rhs_support(self, support_tets, amplitude, out=None):
+        """assemble_rhs(mesh, support_tets, amplitude, total_dofs) (assembly.cpp:335-378),
+        not pinned (as the reference)."""
+        sup = np.ascontiguousarray(np.atleast_1d(support_tets), np.int32)
+        if out is None:
+            out = np.empty(self.n_dofs, np.complex128)
+        _cvec(out, self.n_dofs, "out", writable=True)
+        _check(lib().ect_rhs_support(self.ctx.h, self.h, _ptr(sup), I64(sup.shape[0]),
+                                     D(amplitude), _ptr(out)))
+        return out
+
+    def rhs_region(self, coil_tag, amplitude, out=None):
+        """assemble_rhs(mesh, coil_tag, amplitude, total_dofs) (assembly.cpp:380-384)."""
+        if out is None:
+            out = np.empty(self.n_dofs, np.complex128)
+        _cvec(out, self.n_dofs, "out", writable=True)
+        _check(lib().ect_rhs_region(self.ctx.h, self.h, I32(coil_tag), D(amplitude), _ptr(out)))
+        return out
+
+    def apply_pins_to_rhs(self, rhs):
+        """apply_pins_to_rhs (assembly.cpp:329-333) in place on [n] or [n, k]."""
+        k = 1 if rhs.ndim == 1 else rhs.shape[1]
+        _cvec(rhs, self.n_dofs * k, "rhs", writable=True)
+        _check(lib().ect_apply_pins_to_rhs(self.ctx.h, self.h, _ptr(rhs), I32(k)))
+        return rhs
 
     def delta_impedance(self, primary, reference, xk1, xk2, xl1, xl2):
         arrs = [np.ascontiguousarray(v, np.complex128) if not hasattr(v, "data_ptr") else v
@@ -232,15 +307,20 @@ class Mesh:
 class Matrix:
     """Global CSR system (pattern bit-identical to the reference CSC)."""
 
-    def __init__(self, ctx: Context, mesh: Mesh | None = None, *, csr=None):
+    def __init__(self, ctx: Context, mesh: Mesh | None = None, *, csr=None, csc=None):
+        """From a mesh (K1 pattern; assemble() fills the values), or from
+        external arrays: csr=(row_ptr, col_idx, values) or csc=(col_ptr,
+        row_idx, values) = the reference's CscMatrix (sparse.hpp:56-66)."""
         self.ctx = ctx
         h = VP()
-        if csr is not None:
-            row_ptr, col, val = (np.ascontiguousarray(csr[0], np.int32),
-                                 np.ascontiguousarray(csr[1], np.int32),
-                                 np.ascontiguousarray(csr[2], np.complex128))
-            _check(lib().ect_matrix_from_csr(ctx.h, I64(row_ptr.shape[0] - 1), I64(col.shape[0]),
-                                             _ptr(row_ptr), _ptr(col), _ptr(val), C.byref(h)))
+        ext = csr if csr is not None else csc
+        if ext is not None:
+            ptr, idx, val = (np.ascontiguousarray(ext[0], np.int32),
+                             np.ascontiguousarray(ext[1], np.int32),
+                             np.ascontiguousarray(ext[2], np.complex128))
+            fn = lib().ect_matrix_from_csr if csr is not None else lib().ect_matrix_from_csc
+            _check(fn(ctx.h, I64(ptr.shape[0] - 1), I64(idx.shape[0]), _ptr(ptr), _ptr(idx),
+                      _ptr(val), C.byref(h)))
         else:
             _check(lib().ect_matrix_create(ctx.h, mesh.h, C.byref(h)))
         self.h = h
@@ -254,6 +334,24 @@ class Matrix:
             _lib().ect_matrix_destroy(self.h)
             self.h = None
 
+    @property
+    def symmetric(self) -> bool:
+        v = I32()
+        _check(lib().ect_matrix_symmetric(self.h, C.byref(v)))
+        return bool(v.value)
+
+    def set_preconditioner(self, name: str):
+        _check(lib().ect_matrix_set_preconditioner(self.h, I32(PRECOND[name])))
+        return self
+
+    def precond_info(self) -> dict:
+        """Multigrid hierarchy: levels, setup ms, operator complexity, coarsest n
+        (builds it if needed; zeros for Jacobi)."""
+        v = (D * 4)()
+        _check(lib().ect_matrix_precond_info(self.h, v))
+        return {"levels": int(v[0]), "setup_ms": v[1], "op_complexity": v[2],
+                "coarsest_n": int(v[3])}
+
     def assemble(self, mats: Materials):
         _check(lib().ect_matrix_assemble(self.ctx.h, self.mesh.h, C.byref(mats), self.h))
         return self
@@ -262,7 +360,7 @@ class Matrix:
     def format(self) -> str:
         nb = I32()
         _check(lib().ect_matrix_format(self.h, C.byref(nb)))
-        return {0: "csr", 1: "nb", 2: "nb_tiled", 3: "sell"}[nb.value]
+        return {0: "csr", 1: "nb", 3: "sell"}[nb.value]
 
     def nb_stats(self) -> dict:
         b, c = I64(), I64()
@@ -287,18 +385,20 @@ class Matrix:
     def multiply(self, x, out=None):
         """y = A x (CscMatrix::multiply); x is [n] or [n, k] interleaved."""
         k = 1 if x.ndim == 1 else x.shape[1]
+        xs = _cvec(x, self.n * k, "x")
         if out is None:
-            out = np.empty_like(x) if not hasattr(x, "data_ptr") else x.new_empty(x.shape)
-        xs = x if hasattr(x, "data_ptr") else np.ascontiguousarray(x, np.complex128)
+            out = np.empty_like(xs) if not hasattr(xs, "data_ptr") else xs.new_empty(xs.shape)
+        _cvec(out, self.n * k, "out", writable=True)
         _check(lib().ect_spmv(self.ctx.h, self.h, _ptr(xs), _ptr(out), I32(k)))
         return out
 
     def solve(self, b, tol=1e-8, max_iter=500, restart=80, out=None):
         """solve_iterative replacement: returns (x, [IterResult dicts])."""
         k = 1 if b.ndim == 1 else b.shape[1]
-        bs = b if hasattr(b, "data_ptr") else np.ascontiguousarray(b, np.complex128)
+        bs = _cvec(b, self.n * k, "b")
         if out is None:
-            out = np.empty_like(bs) if not hasattr(b, "data_ptr") else b.new_empty(b.shape)
+            out = np.empty_like(bs) if not hasattr(bs, "data_ptr") else bs.new_empty(bs.shape)
+        _cvec(out, self.n * k, "out", writable=True)
         opts = IterOptions(tol, max_iter, restart)
         res = (IterResult * k)()
         _check(lib().ect_solve(self.ctx.h, self.h, _ptr(bs), _ptr(out), I32(k), C.byref(opts), res))

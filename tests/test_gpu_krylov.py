@@ -49,7 +49,8 @@ def system(ctx):
     g = golden("small_6x6x12")
     mesh = ect.Mesh(ctx, g["xyz"], g["tets"], g["region"])
     p, _, _ = mesh.materials(workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0))
-    a = ect.Matrix(ctx, mesh).assemble(p)  # node-block (NB-E) storage, the default path
+    # node-block (NB-E) storage, the default path; Jacobi: the recurrence numpy restates
+    a = ect.Matrix(ctx, mesh).assemble(p).set_preconditioner("jacobi")
     rp, ci, v = a.export()
     return a, rp, ci, v
 
