@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <chrono>
 #include <complex>
+#include <cstdlib>
 #include <numeric>
 
 #include "ect_internal.h"
@@ -31,7 +32,7 @@
 namespace ect {
 namespace {
 
-constexpr int64_t kDenseMax = 1200;   // coarsest level solved by a dense inverse
+constexpr int64_t kDenseMaxDefault = 1200;  // coarsest level solved by a dense inverse
 constexpr int kMaxLevels = 12;
 constexpr double kPinRatio = 1e6;     // |a_ii| > kPinRatio * sum_{j != i} |a_ij| -> pinned
 
@@ -276,6 +277,15 @@ void amg_setup(ect_matrix* a) {
   if (!a->symmetric) fail(ECT_ERR_SOLVER, "multigrid preconditioner needs a symmetric matrix");
   auto H = std::make_unique<Amg>();
   const int64_t N = a->n;
+  // tuning overrides (experiments; the defaults are the measured choice)
+  auto env_d = [](const char* k, double d) {
+    const char* v = std::getenv(k);
+    return v ? std::atof(v) : d;
+  };
+  const int64_t kDenseMax = (int64_t)env_d("ECT_AMG_DENSE_MAX", (double)kDenseMaxDefault);
+  H->omega = env_d("ECT_AMG_OMEGA", H->omega);
+  H->oc = env_d("ECT_AMG_OC", H->oc);
+  H->wcycle = (int)env_d("ECT_AMG_WCYCLE", H->wcycle);
 
   // ---- finest level: node structure ---------------------------------------
   // from-mesh matrices: node i owns A-dofs 3i..3i+2 and its V-dof; others:
@@ -422,6 +432,13 @@ void amg_setup(ect_matrix* a) {
     std::vector<std::complex<double>> dense(n * n, 0.0), inv;
     for (int64_t r = 0; r < n; ++r)
       for (int p = rp[r]; p < rp[r + 1]; ++p) dense[r * n + cl[p]] = {vl[p].x, vl[p].y};
+    // The constant-V mode of each conductor component is lifted only by the
+    // delta_gauge mass (element_forms.cpp:101-114; ~1e-14 relative)
+    // and survives aggregation, so the coarsest operator is singular to
+    // working precision (cond ~ 1e16 on configs[1]-like meshes). A relative
+    // diagonal shift (1 + reg) keeps its inverse bounded; M stays symmetric.
+    const double reg = env_d("ECT_AMG_REG", 1e-8);
+    for (int64_t r = 0; r < n; ++r) dense[r * n + r] *= 1.0 + reg;
     dense_inverse(n, dense, inv);
     std::vector<double2> h(n * n);
     for (int64_t q = 0; q < n * n; ++q) h[q] = make_double2(inv[q].real(), inv[q].imag());

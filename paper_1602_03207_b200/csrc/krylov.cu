@@ -2144,6 +2144,48 @@ k_dense(int64_t n, const double2* __restrict__ minv, const double2* __restrict__
   }
 }
 
+// rho = r^T z per active column (single-level hierarchy: no smoothing
+// SpMV to fuse it into), finalised by fin_rho
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_rho(int64_t n, const double2* __restrict__ r, const double2* __restrict__ z, KrylovCtl ctl) {
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
+  constexpr int NVL = 2 * CW, NV = 2 * K;
+  __shared__ double smem[32 * NV];
+  if (*ctl.n_active == 0) return;
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  bool act[CW];
+#pragma unroll
+  for (int c = 0; c < CW; ++c) act[c] = ctl.st[kb + c].status == kActive;
+  double part[NVL];
+#pragma unroll
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / KH;
+#pragma unroll
+    for (int c = 0; c < CW; ++c) {
+      if (!act[c]) continue;
+      const int64_t idx = i * K + kb + c;
+      const double2 rv = r[idx], zv = z[idx];
+      part[2 * c] += rv.x * zv.x - rv.y * zv.y;
+      part[2 * c + 1] += rv.x * zv.y + rv.y * zv.x;
+    }
+  }
+  double bsum[NV];
+  block_sum_slots<NVL, KH>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    fin_rho<K>(ctl, tot);
+    *ctl.counter = 0u;
+  }
+}
+
 template <int K>
 struct Cycle {
   using DK = Dispatch<K>;
@@ -2156,7 +2198,9 @@ struct Cycle {
     const int64_t b = (work + kBlock - 1) / kBlock;
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx->num_sms * 8));
   }
+  int grid_vec = 1;                   // <= the partial-buffer rows of the solve
   Cycle(ect_ctx* c, ect_matrix* m, Amg& h) : ctx(c), a(m), H(h) {
+    grid_vec = DK::vec_grid(ctx);
     for (int mode : {kResidNR, kSmooth, kSmoothDot}) grid0[mode] = DK::spmv_grid(ctx, mode, a);
     gl.resize(H.lv.size());
     constexpr int G = K >= 4 ? 8 : 16;
@@ -2203,6 +2247,11 @@ struct Cycle {
       k_dense<K><<<g, kBlock, 0, s>>>(n, H.minv.p, b, out, na);
       CK_LAUNCH();
       note_launch(ctx, 1);
+      if (dot) {  // single-level hierarchy: rho = r^T z here
+        k_rho<K><<<std::min(gvec(n * K), grid_vec), kBlock, 0, s>>>(n, b, out, c);
+        CK_LAUNCH();
+        note_launch(ctx, 1);
+      }
       return;
     }
     c.omega = H.omega;

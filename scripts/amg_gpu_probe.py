@@ -17,6 +17,10 @@ from paper_1602_03207_b200 import ect, workloads  # noqa: E402
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 tol = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-8
 w = workloads.config3()
+if os.environ.get("DIMS"):  # a smaller configs[1]-like box, e.g. DIMS=16,16,32
+    dims = tuple(int(v) for v in os.environ["DIMS"].split(","))
+    w = workloads.Workload("probe", dims, 1, ((0.9, 1.1),), w.physics, workloads._coil(dims[2]),
+                           1e6, w.positions)
 m = w.mesh()
 ctx = ect.Context(0)
 mesh = ect.Mesh(ctx, m.xyz, m.tets, m.region)

@@ -17,7 +17,7 @@ from paper_1602_03207_b200 import workloads
 from paper_1602_03207_b200.workloads import Workload, _coil
 
 
-def cocg(A, b, apply_m, tol=1e-8, max_iter=5000):
+def cocg(A, b, apply_m, tol=1e-8, max_iter=int(__import__("os").environ.get("MAXIT", 5000))):
     x = np.zeros_like(b)
     r = b.copy()
     z = apply_m(r)
@@ -70,7 +70,7 @@ def aggregate(G):
     return agg, na
 
 
-def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=2000, omega_p=2 / 3):
+def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=int(__import__("os").environ.get("COARSE_N", 2000)), omega_p=2 / 3):
     levels = []
     nodes = n_nodes
     # level description: dof_node (node index or -1), dof_kind (0..2 A comp, 3 V)
@@ -108,7 +108,19 @@ def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=2000, omega_p=2 / 
         dof_kind = ukeys % 4
         nodes = n_agg
         free = np.ones(A.shape[0], bool)
-    levels.append({"A": A, "lu": spla.splu(A.tocsc())})
+    import os
+    if os.environ.get("INV"):
+        reg = float(os.environ.get("REG", "0"))
+        Ad = A.toarray()
+        Ad = Ad + reg * np.diag(np.diag(Ad))
+        Minv = np.linalg.inv(Ad)
+        print(f"  coarsest n={A.shape[0]} dense inverse, reg={reg}, cond~{np.linalg.cond(Ad):.2e}", flush=True)
+        class _Inv:
+            def solve(self, b):
+                return Minv @ b
+        levels.append({"A": A, "lu": _Inv()})
+    else:
+        levels.append({"A": A, "lu": spla.splu(A.tocsc())})
     return levels
 
 
@@ -150,15 +162,19 @@ def main():
     b = S.position_rhs(np.array(w.coil), w.positions[0], 1, w.amplitude)
     d = A.diagonal()
     t = time.time()
-    x, it = cocg(A, b, lambda r: r / d)
+    x, it = cocg(A, b, lambda r: r / d) if not __import__("os").environ.get("NOJAC") else (b, 0)
     print(f"jacobi   iters={it:5d} true={np.linalg.norm(b - A @ x) / np.linalg.norm(b):.2e} {time.time()-t:.1f}s", flush=True)
     t = time.time()
     levels = build_levels(A, nn, cond, pins, smooth=smooth)
     print(f"setup {time.time()-t:.1f}s", flush=True)
-    for nu, wj, g, oc in ((1, 0.6, 1, 1.0), (1, 0.6, 2, 1.0), (1, 0.6, 1, 1.5), (1, 0.6, 2, 1.5), (1, 0.6, 1, 2.0)):
+    cfgs = ((1, 0.6, 1, 1.0), (1, 0.6, 2, 1.0), (1, 0.6, 1, 1.5), (1, 0.6, 2, 1.5), (1, 0.6, 1, 2.0))
+    if __import__("os").environ.get("CFGS"):
+        cfgs = [tuple(float(v) for v in c.split(":")) for c in __import__("os").environ["CFGS"].split(",")]
+    for nu, wj, g, oc in cfgs:
+        nu, g = int(nu), int(g)
         t = time.time()
         x, it = cocg(A, b, lambda r: vcycle(levels, r, nu=nu, w=wj, gamma=g, oc=oc))
-        print(f"amg nu={nu} w={wj} gamma={g} oc={oc} iters={it:5d} true={np.linalg.norm(b - A @ x) / np.linalg.norm(b):.2e} {time.time()-t:.1f}s", flush=True)
+        print(f"amg levels={len(levels)} nu={nu} w={wj} gamma={g} oc={oc} iters={it:5d} true={np.linalg.norm(b - A @ x) / np.linalg.norm(b):.2e} {time.time()-t:.1f}s", flush=True)
 
 
 if __name__ == "__main__":

@@ -256,7 +256,7 @@ def test_solver_contracts(ctx):
     g = golden("small_4x4x8")
     A = ref_matrix(g).tocsr()
     A.sort_indices()
-    a = ect.Matrix(ctx, csr=(A.indptr, A.indices, A.data))
+    a = ect.Matrix(ctx, csr=(A.indptr, A.indices, A.data)).set_preconditioner("jacobi")
     x, res = a.solve(np.zeros(a.n, np.complex128))
     assert res[0]["converged"] and res[0]["iterations"] == 0 and np.all(x == 0)
     with pytest.raises(ect.SolverError):
