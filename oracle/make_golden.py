@@ -23,7 +23,10 @@ check parity against committed data:
                  reference's trace format; trace_cfg3.json = per-position
                  checkpoint (iterations, true residuals, solve seconds).
 
-usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|cfg3_trace|all]
+  ref_cost_cfg1.json the reference's GMRES(80)+ILU(0) iteration counts to
+                 1e-8 at two configs[3] positions (bench.py's extrapolation).
+
+usage: python -m oracle.make_golden [small|cfg0|cfg1|cfg3|cfg3_trace|ref_cost|all]
 """
 from __future__ import annotations
 
@@ -275,6 +278,47 @@ def make_cfg3_trace8(indices=CFG3_TRACE8_INDICES, tol=CFG3_TRACE8_TOL,
     print("trace_cfg3.csv complete", f"{time.time() - t0:.0f}s", flush=True)
 
 
+REF_COST_INDICES = (31, 20)
+
+
+def make_ref_cost(indices=REF_COST_INDICES, tol=1e-8, threads=8):
+    """The reference's own iteration count to the benchmark tolerance (SURVEY
+    §8(d) CPU-baseline item 3): solve_iterative (GMRES(80)+ILU(0), the stock
+    IterativeOptions restart, iterative.cpp:109-228) on configs[3] positions of
+    the configs[1] mesh, both coils x both material configurations, each solve
+    accepted on its true residual. bench.py extrapolates the reference's time
+    per probe position from these counts and its measured ILU(0) build and
+    per-iteration times -> ref_cost_cfg1.json."""
+    import os
+    w = workloads.config3()
+    t0 = time.time()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    parts = max(1, os.cpu_count() or 1)
+    its, res, secs = [], [], []
+    for tag, mats in (("primary", prim), ("reference", refm)):
+        s = ref.RefSystem(rm, mats, parts=parts, workers=parts)
+        b = np.stack([s.position_rhs(w.coil, w.positions[i], c, w.amplitude)
+                      for i in indices for c in (1, 2)])
+        out = s.solve_iterative_batch(b, tol=tol, max_iter=20000, restart=80, threads=threads,
+                                      want_x=True)
+        true = [s.relative_residual(out["x"][j], b[j]) for j in range(len(b))]
+        assert max(true) <= tol * 1.01, true
+        its += [int(v) for v in out["iterations"]]
+        res += true
+        secs.append(out["seconds"])
+        print(tag, list(out["iterations"]), f"{out['seconds']:.0f}s", flush=True)
+        del s
+    doc = {"config": "configs[1] mesh, configs[3] positions " + str(list(indices)),
+           "solver": "GMRES(80)+ILU(0) (solve_iterative, IterativeOptions restart 80)",
+           "tol": tol, "iterations": its, "true_residual": res,
+           "order": "per material configuration (primary, reference): positions x coils 1, 2",
+           "solve_wall_s": secs, "threads": threads, "wall_s": time.time() - t0}
+    (GOLDEN / "ref_cost_cfg1.json").write_text(json.dumps(doc, indent=1))
+    print("ref_cost_cfg1.json written", doc, flush=True)
+
+
 TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
 
 
@@ -380,6 +424,8 @@ if __name__ == "__main__":
         make_cfg3_point()
     if what in ("cfg3_trace",):
         make_cfg3_trace8()
+    if what in ("ref_cost",):
+        make_ref_cost()
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):
