@@ -283,36 +283,37 @@ void amg_setup(ect_matrix* a) {
     return v ? std::atof(v) : d;
   };
   const int64_t kDenseMax = (int64_t)env_d("ECT_AMG_DENSE_MAX", (double)kDenseMaxDefault);
+  const double theta = env_d("ECT_AMG_THETA", 0.05);
   H->omega = env_d("ECT_AMG_OMEGA", H->omega);
   H->oc = env_d("ECT_AMG_OC", H->oc);
   H->wcycle = (int)env_d("ECT_AMG_WCYCLE", H->wcycle);
 
-  // ---- finest level: node structure ---------------------------------------
-  // from-mesh matrices: node i owns A-dofs 3i..3i+2 and its V-dof; others:
-  // one node per dof (scalar aggregation of the matrix graph)
-  int64_t n_nodes = N;
-  std::vector<int> dof_node(N), dof_kind(N, 0);
-  std::vector<int64_t> gptr;
+  // ---- level structure: A dofs [0, nA) grouped by node (3 components move
+  // together), scalar V dofs [nA, n) aggregated on their own strength graph:
+  // the V-V couplings are sigma-weighted (element_l22, element_forms.cpp:
+  // 101-114), so a weak conductor between strong ones (the reference
+  // configuration's sigma_eps deposit) separates V aggregates while the A
+  // aggregates (curl-curl + div-div, material-uniform up to mu) cross it.
+  // Matrices without mesh structure: every dof is a scalar A "node".
+  int64_t nA = N, n_anode = N;
+  std::vector<int> a_node, a_kind;  // per A dof
+  std::vector<int64_t> gptr;        // A-node graph
   std::vector<int> gadj;
   if (a->from_mesh && a->mesh && a->mesh->have_nbr) {
     ect_mesh* m = a->mesh;
-    n_nodes = m->n_nodes;
-    const int64_t na = 3 * n_nodes;
-    auto off = download(ctx, m->nbr_off.p, n_nodes + 1);
-    auto nbr = download(ctx, m->nbr.p, (size_t)off[n_nodes]);
-    auto cf = download(ctx, m->cond_fwd.p, n_nodes);
-    for (int64_t i = 0; i < na; ++i) {
-      dof_node[i] = (int)(i / 3);
-      dof_kind[i] = (int)(i % 3);
+    n_anode = m->n_nodes;
+    nA = 3 * n_anode;
+    auto off = download(ctx, m->nbr_off.p, n_anode + 1);
+    auto nbr = download(ctx, m->nbr.p, (size_t)off[n_anode]);
+    a_node.resize(nA);
+    a_kind.resize(nA);
+    for (int64_t i = 0; i < nA; ++i) {
+      a_node[i] = (int)(i / 3);
+      a_kind[i] = (int)(i % 3);
     }
-    for (int64_t i = 0; i < n_nodes; ++i)
-      if (cf[i] >= 0) {
-        dof_node[na + cf[i]] = (int)i;
-        dof_kind[na + cf[i]] = 3;
-      }
-    gptr.assign(n_nodes + 1, 0);
-    gadj.reserve(off[n_nodes]);
-    for (int64_t i = 0; i < n_nodes; ++i) {
+    gptr.assign(n_anode + 1, 0);
+    gadj.reserve(off[n_anode]);
+    for (int64_t i = 0; i < n_anode; ++i) {
       for (int p = off[i]; p < off[i + 1]; ++p)
         if (nbr[p] != (int)i) gadj.push_back(nbr[p]);
       gptr[i + 1] = (int64_t)gadj.size();
@@ -320,7 +321,9 @@ void amg_setup(ect_matrix* a) {
   } else {
     auto rp = download(ctx, a->row_ptr.p, N + 1);
     auto cl = download(ctx, a->col.p, (size_t)a->nnz);
-    std::iota(dof_node.begin(), dof_node.end(), 0);
+    a_node.resize(N);
+    std::iota(a_node.begin(), a_node.end(), 0);
+    a_kind.assign(N, 0);
     gptr.assign(N + 1, 0);
     gadj.reserve(a->nnz);
     for (int64_t i = 0; i < N; ++i) {
@@ -338,27 +341,60 @@ void amg_setup(ect_matrix* a) {
     L.n = A.n;
     L.nnz = A.nnz;
     if (A.n <= kDenseMax || level + 1 >= kMaxLevels) break;
+    const int64_t nV = A.n - nA;
     // free (non-penalty) dofs
     DevBuf<uint8_t> free_d(A.n);
     k_free_rows<<<blocks_for(ctx, A.n), 256, 0, s>>>(A.rp, A.col, A.val, A.n, free_d.p);
     CK_LAUNCH();
     auto free_h = download(ctx, free_d.p, A.n);
+    // A aggregation on the node graph
     std::vector<int> agg;
-    const int64_t n_agg = aggregate(n_nodes, gptr, gadj, agg);
-    // coarse dofs (aggregate, kind) in ascending key order
-    std::vector<int> key_idx(4 * n_agg, -1);
-    for (int64_t i = 0; i < A.n; ++i)
-      if (free_h[i]) key_idx[4 * (int64_t)agg[dof_node[i]] + dof_kind[i]] = 0;
-    int64_t nc = 0;
+    const int64_t n_agg = aggregate(n_anode, gptr, gadj, agg);
+    // V aggregation on the strong V-V couplings |a_ij| >= theta sqrt(|a_ii a_jj|)
+    std::vector<int> aggv;
+    int64_t n_aggv = 0;
+    if (nV > 0) {
+      auto vrp = download(ctx, A.rp + nA, nV + 1);
+      const int base = vrp[0];
+      auto vcl = download(ctx, A.col + base, (size_t)(vrp[nV] - base));
+      auto vvl = download(ctx, A.val + base, (size_t)(vrp[nV] - base));
+      std::vector<double> dv(nV, 0.0);
+      for (int64_t r = 0; r < nV; ++r)
+        for (int p = vrp[r] - base; p < vrp[r + 1] - base; ++p)
+          if (vcl[p] == (int)(nA + r)) dv[r] = std::hypot(vvl[p].x, vvl[p].y);
+      std::vector<int64_t> vptr(nV + 1, 0);
+      std::vector<int> vadj;
+      for (int64_t r = 0; r < nV; ++r) {
+        for (int p = vrp[r] - base; p < vrp[r + 1] - base; ++p) {
+          const int64_t c = (int64_t)vcl[p] - nA;
+          if (c < 0 || c == r) continue;
+          if (std::hypot(vvl[p].x, vvl[p].y) >= theta * std::sqrt(dv[r] * dv[c]))
+            vadj.push_back((int)c);
+        }
+        vptr[r + 1] = (int64_t)vadj.size();
+      }
+      n_aggv = aggregate(nV, vptr, vadj, aggv);
+    }
+    // coarse dofs: A keys (agg, kind) ranked, then V aggregates
+    std::vector<int> key_idx(3 * n_agg, -1);
+    for (int64_t i = 0; i < nA; ++i)
+      if (free_h[i]) key_idx[3 * (int64_t)agg[a_node[i]] + a_kind[i]] = 0;
+    int64_t ncA = 0;
     for (auto& v : key_idx)
+      if (v == 0) v = (int)ncA++;
+    std::vector<int> vidx(n_aggv, -1);
+    for (int64_t r = 0; r < nV; ++r)
+      if (free_h[nA + r]) vidx[aggv[r]] = 0;
+    int64_t nc = ncA;
+    for (auto& v : vidx)
       if (v == 0) v = (int)nc++;
     if (nc == 0 || nc * 5 > A.n * 4) break;  // no useful coarsening: current level is coarsest
     std::vector<int> cmap(A.n, -1), r_ptr(nc + 1, 0), r_idx;
-    for (int64_t i = 0; i < A.n; ++i)
-      if (free_h[i]) {
-        cmap[i] = key_idx[4 * (int64_t)agg[dof_node[i]] + dof_kind[i]];
-        ++r_ptr[cmap[i] + 1];
-      }
+    for (int64_t i = 0; i < A.n; ++i) {
+      if (!free_h[i]) continue;
+      cmap[i] = i < nA ? key_idx[3 * (int64_t)agg[a_node[i]] + a_kind[i]] : vidx[aggv[i - nA]];
+      ++r_ptr[cmap[i] + 1];
+    }
     for (int64_t c = 0; c < nc; ++c) r_ptr[c + 1] += r_ptr[c];
     r_idx.resize(r_ptr[nc]);
     {
@@ -376,20 +412,20 @@ void amg_setup(ect_matrix* a) {
     galerkin(ctx, A, H->lv[H->lv.size() - 2].cmap.p, nc, C);
     nnz_sum += (double)C.nnz;
     A = Csr{C.n, C.nnz, C.row_ptr.p, C.col.p, C.val.p};
-    // coarse node structure: node = aggregate, kind kept
-    std::vector<int> cnode(nc), ckind(nc);
-    for (int64_t k = 0, c = 0; k < 4 * n_agg; ++k)
+    // coarse A-node structure: node = aggregate, kind kept; graph from the
+    // coarse A-A couplings
+    std::vector<int> cnode(ncA), ckind(ncA);
+    for (int64_t k = 0; k < 3 * n_agg; ++k)
       if (key_idx[k] >= 0) {
-        cnode[c] = (int)(k / 4);
-        ckind[c] = (int)(k % 4);
-        ++c;
+        cnode[key_idx[k]] = (int)(k / 3);
+        ckind[key_idx[k]] = (int)(k % 3);
       }
-    auto crp = download(ctx, C.row_ptr.p, nc + 1);
-    auto ccl = download(ctx, C.col.p, (size_t)C.nnz);
+    auto crp = download(ctx, C.row_ptr.p, ncA + 1);
+    auto ccl = download(ctx, C.col.p, (size_t)crp[ncA]);
     std::vector<std::vector<int>> nb(n_agg);
-    for (int64_t r = 0; r < nc; ++r)
+    for (int64_t r = 0; r < ncA; ++r)
       for (int p = crp[r]; p < crp[r + 1]; ++p)
-        if (cnode[ccl[p]] != cnode[r]) nb[cnode[r]].push_back(cnode[ccl[p]]);
+        if (ccl[p] < ncA && cnode[ccl[p]] != cnode[r]) nb[cnode[r]].push_back(cnode[ccl[p]]);
     gptr.assign(n_agg + 1, 0);
     gadj.clear();
     for (int64_t g = 0; g < n_agg; ++g) {
@@ -399,9 +435,10 @@ void amg_setup(ect_matrix* a) {
       gadj.insert(gadj.end(), v.begin(), v.end());
       gptr[g + 1] = (int64_t)gadj.size();
     }
-    n_nodes = n_agg;
-    dof_node = std::move(cnode);
-    dof_kind = std::move(ckind);
+    n_anode = n_agg;
+    nA = ncA;
+    a_node = std::move(cnode);
+    a_kind = std::move(ckind);
   }
   // Jacobi diagonals of every level (level 0: the matrix's own dinv)
   for (size_t l = 1; l < H->lv.size(); ++l) {

@@ -89,6 +89,21 @@ def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=int(__import__("os
         agg, n_agg = aggregate(G)
         # coarse dofs: (aggregate, kind) for every kind present among free dofs
         key = agg[dof_node] * 4 + dof_kind
+        vmode = __import__("os").environ.get("VAGG", "node")
+        isv = dof_kind == 3
+        if vmode == "none":
+            free = free & ~isv
+        elif vmode == "strength" and isv.any():
+            th = float(__import__("os").environ.get("THETA", "0.05"))
+            vi = np.nonzero(isv)[0]
+            AV = A[vi][:, vi].tocsr()
+            dv = np.abs(AV.diagonal())
+            AV = AV.tocoo()
+            strong = (np.abs(AV.data) >= th * np.sqrt(dv[AV.row] * dv[AV.col])) & (AV.row != AV.col)
+            GV = sp.csr_matrix((np.ones(strong.sum()), (AV.row[strong], AV.col[strong])), shape=(len(vi), len(vi)))
+            aggv, nv = aggregate(GV)
+            key = key.copy()
+            key[vi] = (n_agg + aggv) * 4 + 3
         ukeys, cidx = np.unique(key[free], return_inverse=True)
         P0 = sp.csr_matrix((np.ones(free.sum()), (np.nonzero(free)[0], cidx)), shape=(A.shape[0], len(ukeys)))
         if smooth:
@@ -106,7 +121,7 @@ def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=int(__import__("os
         A = Ac
         dof_node = ukeys // 4
         dof_kind = ukeys % 4
-        nodes = n_agg
+        nodes = int(dof_node.max()) + 1
         free = np.ones(A.shape[0], bool)
     import os
     if os.environ.get("INV"):
@@ -151,7 +166,9 @@ def main():
                  _coil(dims[2]), 1e6, (1.0 * workloads.SCALE,))
     mm = w.mesh()
     m = ref.RefMesh(mm.xyz, mm.tets, mm.region)
-    p, _, _ = m.materials(w.physics)
+    p, rr, _ = m.materials(w.physics)
+    if __import__("os").environ.get("CFG") == "ref":
+        p = rr
     t = time.time()
     S = ref.RefSystem(m, p, parts=4, workers=4)
     cp, ri, v, pins = S.export()
