@@ -319,6 +319,60 @@ def make_ref_cost(indices=REF_COST_INDICES, tol=1e-8, threads=8):
     print("ref_cost_cfg1.json written", doc, flush=True)
 
 
+def make_cfg3_trace_batched(indices=CFG3_TRACE8_INDICES, tol=CFG3_TRACE8_TOL,
+                            restart=CFG3_TRACE8_RESTART, threads=None):
+    """make_cfg3_trace8 for a many-core host with memory to spare (the GPU
+    box's 16 cores / 196 GB): each material configuration assembled by the
+    reference with parts = threads (its parallel mode; summation order moves
+    values by ~1e-16 only), then ALL positions' coil right-hand sides solved
+    concurrently, one solve_iterative per host thread (run_scan's parallel_for,
+    scan.cpp:155-156), each accepted on its true residual."""
+    import os
+    threads = threads or (os.cpu_count() or 1)
+    w = workloads.config3()
+    t0 = time.time()
+    mesh = w.mesh()
+    rm = ref.RefMesh(mesh.xyz, mesh.tets, mesh.region)
+    prim, refm, two = rm.materials(w.physics)
+    assert two
+    zs = [w.positions[i] for i in indices]
+    xs, info = {}, {}
+    for tag, mats in (("primary", prim), ("reference", refm)):
+        s = ref.RefSystem(rm, mats, parts=threads, workers=threads)
+        b = np.stack([s.position_rhs(w.coil, z, c, w.amplitude) for z in zs for c in (1, 2)])
+        out = s.solve_iterative_batch(b, tol=tol, max_iter=20000, restart=restart,
+                                      threads=threads, want_x=True)
+        true = [s.relative_residual(out["x"][j], b[j]) for j in range(len(b))]
+        assert max(true) <= tol * 1.01, (tag, true)
+        xs[tag] = out["x"]
+        info[tag] = {"iterations": [int(v) for v in out["iterations"]], "true_residual": true,
+                     "solve_s": out["seconds"]}
+        print(tag, info[tag]["iterations"], f"{out['seconds']:.0f}s solve, "
+              f"{time.time() - t0:.0f}s total", flush=True)
+        del s, b
+    pts = {}
+    for q, i in enumerate(indices):
+        dz = np.array([rm.delta_impedance(prim, refm, xs["primary"][2 * q + k],
+                                          xs["reference"][2 * q + l])
+                       for k in range(2) for l in range(2)])
+        modes = ref.signal_modes(dz)
+        pts[str(i)] = {"z": zs[q], "dz": [[v.real, v.imag] for v in dz],
+                       "modes": [[complex(v).real, complex(v).imag] for v in modes],
+                       "iterations": info["primary"]["iterations"][2 * q:2 * q + 2]
+                       + info["reference"]["iterations"][2 * q:2 * q + 2],
+                       "true_residual": info["primary"]["true_residual"][2 * q:2 * q + 2]
+                       + info["reference"]["true_residual"][2 * q:2 * q + 2]}
+    doc = {"tol": tol, "solver": f"GMRES({restart})+ILU(0)", "mesh": "configs[1]",
+           "assembly_parts": threads, "points": pts, "wall_s": time.time() - t0}
+    (GOLDEN / "trace_cfg3.json").write_text(json.dumps(doc, indent=1))
+    order = sorted(pts.values(), key=lambda p: p["z"])
+    ref.trace_write(GOLDEN / "trace_cfg3.csv", [p["z"] for p in order],
+                    [[complex(*v) for v in p["dz"]] for p in order],
+                    [[complex(*v) for v in p["modes"]] for p in order],
+                    config_hash=f"configs[3] GMRES({restart})+ILU(0) tol {tol:g}")
+    print("trace_cfg3.csv written", f"{time.time() - t0:.0f}s", flush=True)
+
+
 TRACE_Z = (0.0085, 0.0095, 0.0100, 0.0105, 0.0115)
 
 
@@ -426,6 +480,8 @@ if __name__ == "__main__":
         make_cfg3_trace8()
     if what in ("ref_cost",):
         make_ref_cost()
+    if what in ("cfg3_trace_batched",):
+        make_cfg3_trace_batched()
     if what in ("cfg1", "all"):
         make_cfg1()
     if what in ("trace", "all"):

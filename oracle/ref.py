@@ -16,6 +16,8 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "_ref" / "libectref.so"
+# the reference with binding/iterative_gpu.cpp in place of iterative.cpp
+GPU_LIB_PATH = HERE / "_ref" / "libectref_gpu.so"
 REFERENCE_SRC = Path("/root/reference/proj/core/src")
 
 _lib = None
@@ -322,3 +324,44 @@ def trace_max_relative_deviation(a, b):
     out = D()
     _check(lib().ref_trace_max_relative_deviation(str(a).encode(), str(b).encode(), C.byref(out)))
     return out.value
+
+
+def _tube_params(spec: dict) -> np.ndarray:
+    nan = float("nan")
+    box = lambda k: list(spec[k]) if spec.get(k) is not None else [nan] * 4
+    return np.array([spec["domain_radius"], spec["z_min"], spec["z_max"], spec["tube_r_inner"],
+                     spec["tube_r_outer"], spec.get("tube_z_min", nan), spec.get("tube_z_max", nan),
+                     *box("tsp"), *box("defect"), *spec["coil"], spec.get("coil_ref_z", 0.0),
+                     spec.get("resolution", 8), spec.get("outer_radial_grading", 2.0)], np.float64)
+
+
+def scan_session_tube(spec: dict, physics, amplitude, tol, max_iter, restart, gpu=False):
+    """The reference's ScanSession (scan.cpp:27-143, solver.method = iterative)
+    on generate_tube_mesh(spec), solve_position at every spec["scan_z"].
+    gpu=False: the reference's own GMRES(restart)+ILU(0); gpu=True: the same
+    reference code linked with the ectgpu drop-in solve_iterative
+    (oracle/binding/iterative_gpu.cpp, _ref/libectref_gpu.so).
+    Returns [n, 14]: z, dz (8), z_fa (2), z_f3 (2), failed."""
+    L = lib() if not gpu else _gpu_lib()
+    p = _tube_params(spec)
+    zs = np.ascontiguousarray(spec["scan_z"], np.float64)
+    out = np.empty((len(zs), 14))
+    ph = physics_struct(physics)
+    rc = L.ref_scan_session_tube(_p(p, D), _p(zs, D), I32(len(zs)), C.byref(ph), D(amplitude),
+                                 D(tol), I32(max_iter), I32(restart), _p(out, D))
+    if rc != 0:
+        raise RefError(L.ref_last_error().decode())
+    return out
+
+
+_gpu_lib_h = None
+
+
+def _gpu_lib():
+    global _gpu_lib_h
+    if _gpu_lib_h is None:
+        if not GPU_LIB_PATH.exists():
+            raise RefError(f"{GPU_LIB_PATH} not built (make -C oracle)")
+        _gpu_lib_h = C.CDLL(str(GPU_LIB_PATH))
+        _gpu_lib_h.ref_last_error.restype = C.c_char_p
+    return _gpu_lib_h

@@ -216,6 +216,72 @@ int ref_tube_mesh_create(const double* p, const double* scan_z, int32_t n_scan, 
   });
 }
 
+// ScanSession (scan.cpp:27-143) with solver.method = "iterative" on a
+// generated tube mesh (TubeMeshSpec packed as in ref_tube_mesh_create): the
+// reference's own per-position chain with RunConfig defaults otherwise
+// (parts = 1). solve_iterative is the reference's GMRES(restart)+ILU(0) in
+// libectref.so and the ectgpu drop-in (binding/iterative_gpu.cpp) in
+// libectref_gpu.so. out per position: z, dz (8), z_fa (2), z_f3 (2), failed.
+int ref_scan_session_tube(const double* p, const double* scan_z, int32_t n_scan,
+                          const ref_physics* ph, double amplitude, double tol, int32_t max_iter,
+                          int32_t restart, double* out) {
+  return guarded([&] {
+    RunConfig cfg;
+    cfg.mesh_source = "generate";
+    TubeMeshSpec& spec = cfg.geometry;
+    spec.domain_radius = p[0];
+    spec.z_min = p[1];
+    spec.z_max = p[2];
+    spec.tube_r_inner = p[3];
+    spec.tube_r_outer = p[4];
+    if (p[5] == p[5]) spec.tube_z_min = p[5];
+    if (p[6] == p[6]) spec.tube_z_max = p[6];
+    if (p[7] == p[7]) spec.tsp = AnnularBox{p[7], p[8], p[9], p[10]};
+    if (p[11] == p[11]) spec.defect = AnnularBox{p[11], p[12], p[13], p[14]};
+    spec.coil = CoilPair{p[15], p[16], p[17], p[18]};
+    spec.coil_ref_z = p[19];
+    spec.resolution = static_cast<int>(p[20]);
+    spec.outer_radial_grading = p[21];
+    spec.scan_z.assign(scan_z, scan_z + n_scan);
+    cfg.frequency = ph->frequency;
+    cfg.sigma_tube = ph->sigma_tube;
+    cfg.mu_r_tube = ph->mu_r_tube;
+    if (ph->sigma_defect >= 0) cfg.sigma_defect = ph->sigma_defect;
+    if (ph->mu_r_defect >= 0) cfg.mu_r_defect = ph->mu_r_defect;
+    cfg.sigma_eps_ratio = ph->sigma_eps_ratio;
+    cfg.delta_gauge = ph->delta_gauge;
+    cfg.bc_penalty = ph->bc_penalty;
+    cfg.mu_tilde_policy = ph->mu_tilde_harmonic ? "harmonic" : "fixed";
+    cfg.mu_tilde_fixed = ph->mu_tilde_fixed;
+    if (ph->sigma_tsp >= 0) cfg.sigma_tsp = ph->sigma_tsp;
+    if (ph->mu_r_tsp >= 0) cfg.mu_r_tsp = ph->mu_r_tsp;
+    cfg.ibc_tsp = ph->ibc_tsp != 0;
+    cfg.coil_amplitude = amplitude;
+    cfg.parts = 1;
+    cfg.workers = 1;
+    cfg.solver_method = "iterative";
+    cfg.solver_tol = tol;
+    cfg.solver_max_iter = max_iter;
+    cfg.solver_restart = restart;
+    ScanSession session(cfg);
+    for (int32_t i = 0; i < n_scan; ++i) {
+      SignalPoint pt = session.solve_position(scan_z[i]);
+      double* o = out + 14 * i;
+      o[0] = pt.z;
+      for (int k = 0; k < 2; ++k)
+        for (int l = 0; l < 2; ++l) {
+          o[1 + 2 * (2 * k + l)] = pt.delta_z.z[k][l].real();
+          o[2 + 2 * (2 * k + l)] = pt.delta_z.z[k][l].imag();
+        }
+      o[9] = pt.z_fa.real();
+      o[10] = pt.z_fa.imag();
+      o[11] = pt.z_f3.real();
+      o[12] = pt.z_f3.imag();
+      o[13] = pt.failed ? 1.0 : 0.0;
+    }
+  });
+}
+
 // load_mesh / write_mesh (mesh_io.cpp), canonical tag map
 int ref_mesh_load(const char* path, void** out) {
   return guarded([&] {

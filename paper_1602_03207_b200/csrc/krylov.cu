@@ -542,6 +542,108 @@ __device__ __forceinline__ int2 ldg_i2(const int2* p) {
   return v;
 }
 
+// Multi-RHS CSR SpMV with column-pair lanes (K >= 2; coarse multigrid levels,
+// CSR / IBC matrices): G = (K/2) x E lanes per row, lane (e, c) streams the
+// row's entries e, e + E, ... and gathers the 2 right-hand sides 2c, 2c + 1
+// of each column with one 256-bit load; the E entry lanes reduce by shuffles.
+// Same epilogues as k_spmv.
+template <int K, int E, int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_spmv_v(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col,
+         const double2* __restrict__ val, const double2* __restrict__ x, double2* __restrict__ y,
+         const double2* __restrict__ b, KrylovCtl ctl) {
+  static_assert(K % 2 == 0, "column pairs");
+  constexpr int CLN = K / 2, G = CLN * E, RPW = 32 / G;
+  static_assert(32 % G == 0, "lanes per row");
+  constexpr int NVL0 = mode_nv(MODE, 2), NVL = NVL0 > 0 ? NVL0 : 1;
+  constexpr int NV = NVL * CLN;
+  __shared__ double smem[32 * NV];
+  if (MODE != kPlain && *ctl.n_active == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G, e = g / CLN, cl = g % CLN, kc = 2 * cl;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part[NVL];
+#pragma unroll
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
+  for (int64_t wrow = warp * RPW; wrow < n; wrow += n_warps * RPW) {
+    const int64_t row = wrow + lane / G;
+    const bool valid = row < n;
+    const int beg = valid ? row_ptr[row] : 0, end = valid ? row_ptr[row + 1] : 0;
+    double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    for (int p = beg + e; p < end; p += E) {
+      const int j = ldg_i(col + p);
+      const double2 a = ldg2(val + p);
+      double2 x0, x1;
+      ld4x(x + (int64_t)j * K + kc, x0, x1);
+      acc[0].x += a.x * x0.x - a.y * x0.y;
+      acc[0].y += a.x * x0.y + a.y * x0.x;
+      acc[1].x += a.x * x1.x - a.y * x1.y;
+      acc[1].y += a.x * x1.y + a.y * x1.x;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int o = G / 2; o >= CLN; o >>= 1) {
+        acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, o, G);
+        acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, o, G);
+      }
+    if (e == 0 && valid) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t idx = row * K + kc + c;
+        const double2 v = acc[c];
+        if (MODE == kPlain) {
+          y[idx] = v;
+        } else if (MODE == kCocg) {
+          y[idx] = v;
+          const double2 pv = x[idx];
+          part[2 * c] += pv.x * v.x - pv.y * v.y;
+          part[2 * c + 1] += pv.x * v.y + pv.y * v.x;
+        } else if (MODE == kResid) {
+          const double2 rv = csub(b[idx], v);
+          y[idx] = rv;
+          part[c] += rv.x * rv.x + rv.y * rv.y;
+        } else if (MODE == kResidNR) {
+          y[idx] = csub(b[idx], v);
+        } else {
+          const double2 bv = b[idx];
+          const double2 d = ctl.dinv[row];
+          const double2 zv = cadd(x[idx], cmul(make_double2(ctl.omega * d.x, ctl.omega * d.y),
+                                               csub(bv, v)));
+          y[idx] = zv;
+          if (MODE == kSmoothDot) {
+            part[2 * c] += bv.x * zv.x - bv.y * zv.y;
+            part[2 * c + 1] += bv.x * zv.y + bv.y * zv.x;
+          }
+        }
+      }
+    }
+  }
+  if (NVL0 == 0) return;
+  double bsum[NV];
+  block_sum_slots<NVL, CLN>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    if (ctl.red) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) ctl.red[j] = tot[j];
+    } else if (MODE == kCocg) {
+      fin_alpha<K>(ctl, tot);
+    } else if (MODE == kSmoothDot) {
+      fin_rho<K>(ctl, tot);
+    } else {
+      fin_resid<K>(ctl, tot);
+    }
+    *ctl.counter = 0u;
+  }
+}
+
 // ---- SELL-C-sigma SpMV (configs[2]'s storage comparison) -------------------------
 // Rows sorted by length (descending) inside windows of sigma rows, then cut
 // into chunks of C = 32 rows (one warp); a chunk stores its entries column-
@@ -710,9 +812,9 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
   const int g = lane & (G - 1);
   const int bl = g / CL, cl = g % CL;
   const int kc = cl * KL;      // first column of this lane
-  bool act[KL];
-#pragma unroll
-  for (int k = 0; k < KL; ++k) act[k] = (MODE == kPlain) || ctl.st[kc + k].status == kActive;
+  // every column is computed (no per-column predicates in the block loop):
+  // frozen columns' outputs are scratch and their partial sums are ignored by
+  // the finalisations, which only touch active columns
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t na = A.na;
@@ -806,7 +908,6 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
         constexpr int KP = (KL % 2 == 0) ? 2 : 1;
 #pragma unroll
         for (int k0 = 0; k0 < KL; k0 += KP) {
-          if (!act[k0] && !act[k0 + KP - 1]) continue;
           double2 xp[3][KP];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
@@ -844,7 +945,6 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           constexpr int KP = (KL % 2 == 0) ? 2 : 1;
 #pragma unroll
           for (int k0 = 0; k0 < KL; k0 += KP) {
-            if (!act[k0] && !act[k0 + KP - 1]) continue;
             double2 xa[3][KP], xv[KP];
             if constexpr (KP == 2) {
               ld4x(xvp + k0, xv[0], xv[1]);
@@ -895,7 +995,6 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
     if (bl == 0 && valid) {
 #pragma unroll
       for (int k = 0; k < KL; ++k) {
-        if (!act[k]) continue;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (c == 3 && cf_i < 0) break;
@@ -1100,7 +1199,8 @@ struct VecMap {
 template <int K, bool EXT = false>
 __global__ void __launch_bounds__(kBlock)
 k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
-         const double2* __restrict__ dinv, KrylovCtl ctl) {
+         const double2* __restrict__ dinv, KrylovCtl ctl, double2* __restrict__ xt = nullptr,
+         double omega = 0.0) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
   constexpr int PV = EXT ? 1 : 3;  // values per column
   constexpr int NVL = PV * CW, NV = PV * K;
@@ -1122,7 +1222,7 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
-    const double2 d = EXT ? make_double2(0.0, 0.0) : dinv[i];
+    const double2 d = (EXT && !xt) ? make_double2(0.0, 0.0) : dinv[i];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
       if (!act[c]) continue;
@@ -1131,6 +1231,8 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
       r[idx] = rv;
       if constexpr (EXT) {
         part[c] += rv.x * rv.x + rv.y * rv.y;
+        // the multigrid cycle's first step on the finest level, x = omega D^-1 r
+        if (xt) xt[idx] = cmul(make_double2(omega * d.x, omega * d.y), rv);
       } else {
         const double2 z = cmul(d, rv);
         part[3 * c] += rv.x * z.x - rv.y * z.y;
@@ -1328,18 +1430,25 @@ const void* nbe_fn(int mode) {
     default: return nbe_kernel<K, kSmoothDot>();
   }
 }
+template <int K, int MODE>
+const void* csr_kernel() {
+  if constexpr (K == 1) return (const void*)k_spmv<16, 1, MODE>;
+  else return (const void*)k_spmv_v<K, (K >= 16 ? 1 : 16 / K), MODE>;
+}
 template <int K>
 const void* csr_fn(int mode) {
-  constexpr int G = K >= 4 ? 8 : 16;
   switch (mode) {
-    case kPlain: return (const void*)k_spmv<G, K, kPlain>;
-    case kCocg: return (const void*)k_spmv<G, K, kCocg>;
-    case kResid: return (const void*)k_spmv<G, K, kResid>;
-    case kResidNR: return (const void*)k_spmv<G, K, kResidNR>;
-    case kSmooth: return (const void*)k_spmv<G, K, kSmooth>;
-    default: return (const void*)k_spmv<G, K, kSmoothDot>;
+    case kPlain: return csr_kernel<K, kPlain>();
+    case kCocg: return csr_kernel<K, kCocg>();
+    case kResid: return csr_kernel<K, kResid>();
+    case kResidNR: return csr_kernel<K, kResidNR>();
+    case kSmooth: return csr_kernel<K, kSmooth>();
+    default: return csr_kernel<K, kSmoothDot>();
   }
 }
+// lanes per row of the CSR kernel (grid sizing)
+template <int K>
+constexpr int csr_lanes() { return K == 1 ? 16 : (K / 2) * (K >= 16 ? 1 : 16 / K); }
 template <int K>
 const void* sell_fn(int mode) {
   return mode == kPlain  ? (const void*)k_sell_spmv<K, kPlain>
@@ -2203,7 +2312,7 @@ struct Cycle {
     grid_vec = DK::vec_grid(ctx);
     for (int mode : {kResidNR, kSmooth, kSmoothDot}) grid0[mode] = DK::spmv_grid(ctx, mode, a);
     gl.resize(H.lv.size());
-    constexpr int G = K >= 4 ? 8 : 16;
+    constexpr int G = csr_lanes<K>();
     for (size_t l = 1; l < H.lv.size(); ++l)
       for (int mode : {kResidNR, kSmooth}) {
         const int64_t need = (H.lv[l].n * G + kBlock - 1) / kBlock;
@@ -2235,8 +2344,10 @@ struct Cycle {
       DK::csr(ctx, mode, gl[l][mode], L.n, L.row_ptr.p, L.col.p, L.val.p, x, y, b, c);
     }
   }
-  // out = M_l b; t0 = a free level-0 vector (COCG's q)
-  void run(size_t l, const double2* b, double2* out, double2* t0, KrylovCtl c, bool dot) {
+  // out = M_l b; t0 = a free level-0 vector (COCG's q); pre = the level's
+  // x = omega D^-1 b is already in xt (fused into the COCG update)
+  void run(size_t l, const double2* b, double2* out, double2* t0, KrylovCtl c, bool dot,
+           bool pre = false) {
     cudaStream_t s = ctx->stream;
     AmgLevel& L = H.lv[l];
     const int64_t n = L.n;
@@ -2258,8 +2369,10 @@ struct Cycle {
     const double2* dinv = l == 0 ? a->dinv.p : L.dinv.p;
     double2* xt = L.xt.p;
     double2* t = l == 0 ? t0 : L.t.p;
-    k_vscale<K><<<gvec(n * K), kBlock, 0, s>>>(n, b, dinv, H.omega, xt, na);
-    CK_LAUNCH();
+    if (!pre) {
+      k_vscale<K><<<gvec(n * K), kBlock, 0, s>>>(n, b, dinv, H.omega, xt, na);
+      CK_LAUNCH();
+    }
     spmv(l, kResidNR, xt, t, b, c);
     AmgLevel& C = H.lv[l + 1];
     k_restrict<K><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, L.r_ptr.p, L.r_idx.p, t, C.b.p, na);
@@ -2400,13 +2513,15 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
           // same sampled iterations as the SpMV, same active-column snapshot
           if (ev[0]) prof_begin(ctx, ev2, 1, false, nullptr, k, prof_snap_of(ctx, ev[0]));
           if (ext) {
-            k_update<KW, true><<<grid_v, kBlock, 0, s>>>(n, r.p, q.p, nullptr, ctl);
+            const bool fuse = a->amg->lv.size() > 1;
+            k_update<KW, true><<<grid_v, kBlock, 0, s>>>(
+                n, r.p, q.p, a->dinv.p, ctl, fuse ? a->amg->lv[0].xt.p : nullptr, a->amg->omega);
             CK_LAUNCH();
             prof_end(ctx, ev2);
             cudaEvent_t ev3[2];
             ev3[0] = ev3[1] = nullptr;
             if (ev[0]) prof_begin(ctx, ev3, 2, false, nullptr, k, prof_snap_of(ctx, ev[0]));
-            cyc->run(0, r.p, W.z.p, q.p, ctl, true);  // z = M r, rho, beta
+            cyc->run(0, r.p, W.z.p, q.p, ctl, true, fuse);  // z = M r, rho, beta
             prof_end(ctx, ev3);
             k_pupdate<KW, true><<<grid_v, kBlock, 0, s>>>(n, xx.p, r.p, p.p, nullptr, ctl, W.z.p);
             CK_LAUNCH();
