@@ -348,6 +348,14 @@ int ect_comm_destroy(ect_comm* c);
  * G, Vo, Vg, n_peers, n_blocks. */
 int ect_part_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix* m, const int64_t* splits,
                     int32_t n_parts, int32_t part, ect_part** out);
+/* The same part without a global matrix: only the slab's rows are patterned
+ * and assembled on this GPU (K1 + K2 over nodes [splits[part], splits[part+1]),
+ * the reference's per-partition assembly, assembly.cpp:246-258), so device
+ * memory per rank is the slab's share of the matrix. Bit-identical blocks to
+ * ect_part_create on the assembled global matrix. */
+int ect_part_create_assembled(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* mats,
+                              const int64_t* splits, int32_t n_parts, int32_t part,
+                              ect_part** out);
 int ect_part_destroy(ect_part* p);
 int ect_part_info(ect_part* p, int64_t info[8]);
 /* Partitioned Jacobi-COCG on GLOBAL b/x ([n][n_rhs]); each part reads and

@@ -287,6 +287,7 @@ void amg_setup(ect_matrix* a) {
   H->omega = env_d("ECT_AMG_OMEGA", H->omega);
   H->oc = env_d("ECT_AMG_OC", H->oc);
   H->wcycle = (int)env_d("ECT_AMG_WCYCLE", H->wcycle);
+  H->f32 = env_d("ECT_AMG_F32", 1.0) != 0.0;
 
   // ---- level structure: A dofs [0, nA) grouped by node (3 components move
   // together), scalar V dofs [nA, n) aggregated on their own strength graph:

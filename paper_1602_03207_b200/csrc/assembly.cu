@@ -109,7 +109,7 @@ k_assemble(const int4* __restrict__ tets, const uint8_t* __restrict__ region,
            const int* __restrict__ nbr, const uint8_t* __restrict__ nbr_cond,
            const int* __restrict__ cond_fwd, const uint8_t* __restrict__ pinned,
            const int* __restrict__ row_ptr, int64_t n_nodes, AsmParams P, double2* val,
-           int* err) {
+           int* err, int64_t lo, int64_t hi) {
   __shared__ TetSlot slots[kWarps][32];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -118,7 +118,7 @@ k_assemble(const int4* __restrict__ tets, const uint8_t* __restrict__ region,
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = (int)(3 * n_nodes);
 
-  for (int64_t i = warp; i < n_nodes; i += n_warps) {
+  for (int64_t i = lo + warp; i < hi; i += n_warps) {
     const int ib = inc_off[i], deg = inc_off[i + 1] - ib;
     const int nb = nbr_off[i], u = nbr_off[i + 1] - nb;
     int ncc = 0;
@@ -439,14 +439,15 @@ void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a) {
   }
   DevBuf<int> err(1);
   CK(cudaMemsetAsync(err.p, 0, sizeof(int), s));
-  int64_t blocks = (m->n_nodes + kWarps - 1) / kWarps;
+  const int64_t lo = a->node_lo, hi = a->node_hi < 0 ? m->n_nodes : a->node_hi;
+  int64_t blocks = (hi - lo + kWarps - 1) / kWarps;
   int64_t cap = (int64_t)ctx->num_sms * 8;
   if (blocks > cap) blocks = cap;
   auto kern = ibc ? k_assemble<true> : k_assemble<false>;
   kern<<<(int)blocks, kWarps * 32, 0, s>>>(m->tets.p, m->region.p, m->xyz.p, m->inc_off.p,
                                           m->inc.p, m->nbr_off.p, m->nbr.p, m->nbr_cond.p,
                                           m->cond_fwd.p, m->pinned.p, a->row_ptr.p, m->n_nodes, P,
-                                          a->val.p, err.p);
+                                          a->val.p, err.p, lo, hi);
   CK_LAUNCH();
   note_launch(ctx, 1);
   int h_err = 0;
@@ -456,6 +457,7 @@ void assemble_values(ect_mesh* m, const ect_materials& mats, ect_matrix* a) {
   a->assembled = true;
   a->symmetric = !ibc;  // element_ibc: va = i omega av^T
   compute_jacobi(a);
+  if (a->node_lo > 0 || (a->node_hi >= 0 && a->node_hi < m->n_nodes)) return;  // slab: see create_part_assembled
   if (ctx->use_sell) build_sell(a, ctx->sell_sigma);
   else if (!ctx->force_csr) build_nb(m, a);
 }

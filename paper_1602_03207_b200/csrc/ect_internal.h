@@ -114,6 +114,11 @@ struct Amg {
   int kcap = 0;                      // batch width the work vectors hold
   double setup_ms = 0.0;
   double op_complexity = 0.0;        // sum of level nnz / fine nnz
+  // finest-level smoothing in fp32 (krylov.cu k_nbe32): NB-E block / coupling
+  // copies and the level's iterate and residual
+  bool f32 = true;
+  DevBuf<float> blk32, cpl32;
+  DevBuf<float2> xt32, t32;
 };
 
 }  // namespace ect
@@ -190,6 +195,7 @@ struct ect_matrix {
   int precond = ECT_PRECOND_JACOBI;  // ECT_PRECOND_* used by ect_solve / the session
   std::unique_ptr<ect::Amg> amg;    // built on first use of ECT_PRECOND_AMG
   int64_t n_zero_diag = 0;          // Jacobi: rows without a usable diagonal
+  int64_t node_lo = 0, node_hi = -1;  // rows of these nodes only (slab), -1: all
   int64_t n = 0, nnz = 0;
   int64_t n_nodes = 0, n_cond = 0;  // DOF structure when built from a mesh
   bool from_mesh = false;
@@ -208,7 +214,7 @@ struct ect_matrix {
   const int* nb_blk_ptr = nullptr;  // = mesh->nbr_off (borrowed)
   const int* nb_blk_col = nullptr;  // = mesh->nbr (borrowed)
   const int* nb_cond_fwd = nullptr; // = mesh->cond_fwd (borrowed)
-  ect::DevBuf<double2> nb_blk;      // [6][nb_blocks]
+  ect::DevBuf<double2> nb_blk;      // [6][nb_blocks] (released once NB-E is built)
   ect::DevBuf<int> nb_cpl_ptr;      // n_nodes + 1
   ect::DevBuf<int2> nb_cpl_idx;     // (node m, cond dof of m)
   ect::DevBuf<double2> nb_cpl;      // [4][nb_cpl]
@@ -232,9 +238,9 @@ struct ect_part {
   ect::HaloPlan plan;
   int64_t n_global = 0, na_global = 0, n_nodes_global = 0;
   int64_t nblk = 0, ncpl = 0;
-  ect::DevBuf<int> blk_ptr, blk_col, cpl_ptr, cond_local;
+  ect::DevBuf<int> blk_ptr, cpl_ptr, cond_local;
   ect::DevBuf<int2> cpl_idx;
-  ect::DevBuf<double2> blk, cpl, dinv;  // NB planes (3 x 4 doubles, 2 x 4 doubles), local dinv
+  ect::DevBuf<double2> cpl, dinv;  // coupling planes (2 x 4 doubles), local dinv
   int64_t int_lo = 0, int_hi = 0;        // interior owned nodes (no ghost columns)
   bool has_nbe = false;                  // sliced-ELL copy of blk (default SpMV layout)
   int64_t nbe_slots = 0;
@@ -261,7 +267,9 @@ bool is_device_ptr(const void* p);
 
 // Kernel entry points implemented in the .cu files.
 void build_mesh_topology(ect_mesh* m);                         // mesh.cu
-void build_pattern(ect_mesh* m, ect_matrix* a);                // pattern.cu
+// K1 pattern; rows of nodes [lo, hi) only when a range is given (slab of a
+// row partition: the other rows stay empty, indices stay global)
+void build_pattern(ect_mesh* m, ect_matrix* a, int64_t lo = 0, int64_t hi = -1);  // pattern.cu
 void export_csc_values(ect_matrix* a, double2* out);           // pattern.cu (symmetric pattern)
 // External CSC (csc = true) or CSR arrays on the device -> a's CSR + symmetry probe
 void matrix_from_compressed(ect_ctx* ctx, int64_t n, int64_t nnz, const int* ptr, const int* idx,
@@ -293,6 +301,9 @@ void amg_setup(ect_matrix* a);                                  // amg.cu
 
 // distributed solve (krylov.cu)
 ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_parts, int part);
+// the same part assembled directly: only the slab's rows are ever built
+ect_part* create_part_assembled(ect_mesh* m, const ect_materials& mats, const int64_t* splits,
+                                int n_parts, int part);
 void dist_solve(ect_part** parts, int n_parts, ect_comm* comm, const double2* b_global,
                 double2* x_global, int k, const ect_iter_options& opt, SolveOut* out);
 // NCCL entry points resolved at runtime (ectgpu.cpp)

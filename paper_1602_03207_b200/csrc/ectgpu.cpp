@@ -1245,6 +1245,22 @@ int ect_part_create(ect_ctx* ctx, ect_mesh* mesh, ect_matrix* a, const int64_t* 
   });
 }
 
+int ect_part_create_assembled(ect_ctx* ctx, ect_mesh* mesh, const ect_materials* mats,
+                              const int64_t* splits, int32_t n_parts, int32_t part,
+                              ect_part** out) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    ScopedDevice sd(ctx->device);
+    check_materials(*mats);
+    try {
+      EventTimer t(ctx, &ctx->timings.assemble_ms);
+      *out = ect::create_part_assembled(mesh, *mats, splits, n_parts, part);
+    } catch (const std::invalid_argument& e) {
+      ect::fail(ECT_ERR_CONFIG, e.what());
+    }
+  });
+}
+
 int ect_part_destroy(ect_part* p) {
   return guarded([&] {
     if (!p) return;

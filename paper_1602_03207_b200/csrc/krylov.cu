@@ -42,6 +42,13 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
 __device__ __forceinline__ double2 csub(double2 a, double2 b) {
   return make_double2(a.x - b.x, a.y - b.y);
 }
+// fp64 <-> fp32 complex element access (multigrid work vectors)
+__device__ __forceinline__ double2 as_d2(double2 v) { return v; }
+__device__ __forceinline__ double2 as_d2(float2 v) { return make_double2(v.x, v.y); }
+__device__ __forceinline__ void put(double2* p, double2 v) { *p = v; }
+__device__ __forceinline__ void put(float2* p, double2 v) {
+  *p = make_float2((float)v.x, (float)v.y);
+}
 // Smith's complex division a / b
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   if (fabs(b.x) >= fabs(b.y)) {
@@ -1060,12 +1067,14 @@ __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __res
                            const int* __restrict__ nbr_off, const int* __restrict__ nbr,
                            const uint8_t* __restrict__ nbr_cond, const int* __restrict__ cond_fwd,
                            const int* __restrict__ cpl_ptr, int64_t n_nodes, double* blk,
-                           int64_t nblk, int2* cpl_idx, double* cpl, int64_t ncpl, int* bad) {
+                           int64_t nblk, int2* cpl_idx, double* cpl, int64_t ncpl, int* bad,
+                           int64_t lo, int64_t hi, int64_t blk_base, int64_t cpl_base) {
+  // nodes [lo, hi); block q / coupling p stored at q - blk_base / p - cpl_base
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t na = 3 * n_nodes;
-  for (int64_t i = warp; i < n_nodes; i += n_warps) {
+  for (int64_t i = lo + warp; i < hi; i += n_warps) {
     const int nb = nbr_off[i], u = nbr_off[i + 1] - nb;
     const int cf_i = cond_fwd[i];
     int ncc = 0;
@@ -1095,7 +1104,7 @@ __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __res
           Bv[c][d] = v.x;
           if (c == d) Im[c] = v.y; else nonzero_offdiag_im |= v.y != 0.0;
         }
-      const int64_t q = nb + r;
+      const int64_t q = nb + r - blk_base;
       const double w0[4] = {Bv[0][0], Bv[0][1], Bv[0][2], Bv[1][0]};
       const double w1[4] = {Bv[1][1], Bv[1][2], Bv[2][0], Bv[2][1]};
       const double w2[4] = {Bv[2][2], Im[0], Im[1], Im[2]};
@@ -1107,7 +1116,7 @@ __global__ void k_build_nb(const int* __restrict__ row_ptr, const double2* __res
       }
       if (mc) {
         const int m = nbr[nb + r];
-        const int64_t p = cb + rc;
+        const int64_t p = cb + rc - cpl_base;
         double av[3], va[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -1170,9 +1179,41 @@ __global__ void k_nbe_fill(const int* __restrict__ blk_ptr, const int* __restric
   }
 }
 
+// A part's NB-E slots straight from the global NB-E: local node il = global
+// n0 + il, its block j read from the global slot of (n0 + il, j), columns
+// mapped global -> local (g2l); padding slots are zero blocks on the node itself.
+__global__ void k_part_nbe_fill(const int* __restrict__ lptr, int64_t L, int64_t n0,
+                                const int* __restrict__ goff, const int* __restrict__ gcol,
+                                const double* __restrict__ gblk, int64_t gslots,
+                                const int* __restrict__ g2l, const int* __restrict__ loff,
+                                int64_t n_chunks, int* __restrict__ lcol,
+                                double* __restrict__ lblk, int64_t lslots) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 32 * n_chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t >> 5, il = t;
+    const int l = (int)(t & 31);
+    const int o = loff[c], w = (loff[c + 1] - o) >> 5;
+    const bool node = il < L;
+    const int deg = node ? lptr[il + 1] - lptr[il] : 0;
+    const int64_t i = n0 + il;
+    const int64_t gs0 = node ? goff[i >> 5] + (i & 31) : 0;
+    for (int j = 0; j < w; ++j) {
+      const int64_t sl = o + 32 * (int64_t)j + l;
+      const bool real = j < deg;
+      const int64_t gs = gs0 + 32 * (int64_t)j;
+      lcol[sl] = real ? g2l[gcol[gs]] : (node ? (int)il : 0);
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          lblk[4 * (pl * lslots + sl) + e] = real ? gblk[4 * (pl * gslots + gs) + e] : 0.0;
+    }
+  }
+}
+
 __global__ void k_cpl_count(const int* __restrict__ nbr_off, const uint8_t* __restrict__ nbr_cond,
-                            const int* __restrict__ cond_fwd, int64_t n_nodes, int* cnt) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
+                            const int* __restrict__ cond_fwd, int64_t lo, int64_t hi, int* cnt) {
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
        i += (int64_t)gridDim.x * blockDim.x) {
     int c = 0;
     if (cond_fwd[i] >= 0)
@@ -1200,7 +1241,7 @@ template <int K, bool EXT = false>
 __global__ void __launch_bounds__(kBlock)
 k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
          const double2* __restrict__ dinv, KrylovCtl ctl, double2* __restrict__ xt = nullptr,
-         double omega = 0.0) {
+         double omega = 0.0, float2* __restrict__ xt32 = nullptr) {
   constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
   constexpr int PV = EXT ? 1 : 3;  // values per column
   constexpr int NVL = PV * CW, NV = PV * K;
@@ -1222,7 +1263,7 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / KH;
     const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);  // owned rows
-    const double2 d = (EXT && !xt) ? make_double2(0.0, 0.0) : dinv[i];
+    const double2 d = (EXT && !xt && !xt32) ? make_double2(0.0, 0.0) : dinv[i];
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
       if (!act[c]) continue;
@@ -1233,6 +1274,7 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
         part[c] += rv.x * rv.x + rv.y * rv.y;
         // the multigrid cycle's first step on the finest level, x = omega D^-1 r
         if (xt) xt[idx] = cmul(make_double2(omega * d.x, omega * d.y), rv);
+        if (xt32) put(xt32 + idx, cmul(make_double2(omega * d.x, omega * d.y), rv));
       } else {
         const double2 z = cmul(d, rv);
         part[3 * c] += rv.x * z.x - rv.y * z.y;
@@ -1667,8 +1709,8 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
   DevBuf<int> cnt(nn + 1);
   CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), s));
   const int grid = (int)std::min<int64_t>((nn + 255) / 256, (int64_t)ctx->num_sms * 16);
-  k_cpl_count<<<std::max(grid, 1), 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p, m->cond_fwd.p, nn,
-                                                 cnt.p);
+  k_cpl_count<<<std::max(grid, 1), 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p, m->cond_fwd.p, 0,
+                                                 nn, cnt.p);
   CK_LAUNCH();
   a->nb_cpl_ptr.alloc(nn + 1);
   size_t tmp = 0;
@@ -1693,7 +1735,7 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
                                                  reinterpret_cast<double*>(a->nb_blk.p), nblk,
                                                  a->nb_cpl_idx.p,
                                                  reinterpret_cast<double*>(a->nb_cpl.p),
-                                                 ncpl, bad.p);
+                                                 ncpl, bad.p, 0, nn, 0, 0);
   CK_LAUNCH();
   note_launch(ctx, 3);
   int h_bad = 0;
@@ -1733,6 +1775,8 @@ void build_nb(ect_mesh* m, ect_matrix* a) {
     CK(cudaStreamSynchronize(s));
     a->nbe_slots = slots;
     a->has_nbe = true;
+    // only the sliced-ELL copy stays resident (parts are cut from it too)
+    a->nb_blk.release();
   }
 }
 
@@ -2157,6 +2201,235 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
 
 }  // namespace
 
+// ---- single-precision finest-level smoothing (multigrid cycle) -----------------
+// The damped-Jacobi sweeps of the finest level only have to reduce the error's
+// oscillatory part, so they stream an fp32 copy of the NB-E blocks and fp32
+// iterates: half the bytes of the two smoothing SpMVs and of the cycle's
+// finest-level vectors. The residual b = r, D^-1, the output z = M r and the
+// dot r^T z stay fp64 (the COCG recurrence is untouched). Measured on a
+// configs[1]-like mesh: 62 -> 62 iterations to 1e-8, 104 -> 107 to 1e-12.
+struct Nb32 {
+  const int* e_off;
+  const int* blk_col;
+  const float* blk;  // plane p of slot q at blk + 4 * (p * nslots + q): 9 real + 3 diag imag
+  int64_t nslots;
+  const int* cpl_ptr;
+  const int2* cpl_idx;
+  const float* cpl;  // plane p of coupling q at cpl + 4 * (p * ncpl + q)
+  int64_t ncpl;
+  const int* cond_fwd;
+  int64_t n_nodes, na;
+};
+
+__device__ __forceinline__ void ld4f(const float* p, float (&v)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld2xf(const float2* p, float2& a, float2& b) {
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y)
+               : "l"(p));
+}
+
+__device__ __forceinline__ void load_block32(const Nb32& A, int64_t q, float (&B)[3][3],
+                                             float (&Im)[3]) {
+  float v0[4], v1[4], v2[4];
+  ld4f(A.blk + 4 * q, v0);
+  ld4f(A.blk + 4 * (A.nslots + q), v1);
+  ld4f(A.blk + 4 * (2 * A.nslots + q), v2);
+  B[0][0] = v0[0]; B[0][1] = v0[1]; B[0][2] = v0[2];
+  B[1][0] = v0[3]; B[1][1] = v1[0]; B[1][2] = v1[1];
+  B[2][0] = v1[2]; B[2][1] = v1[3]; B[2][2] = v2[0];
+  Im[0] = v2[1]; Im[1] = v2[2]; Im[2] = v2[3];
+}
+
+// K right-hand sides, G = GB x CL lanes per node (block lanes x column lanes,
+// KL = K / CL columns per lane, even or 1). Modes:
+//  kResidNR  : y32 = b - A x                  (b fp64, x fp32, y fp32)
+//  kSmoothDot: z = x + omega D^-1 (b - A x), rho partials b^T z (z fp64)
+template <int G, int K, int MODE, int MINB, int CL>
+__global__ void __launch_bounds__(kBlock, MINB)
+k_nbe32(Nb32 A, const float2* __restrict__ x, void* __restrict__ yv,
+        const double2* __restrict__ b, KrylovCtl ctl) {
+  static_assert(G % CL == 0 && K % CL == 0, "lane split");
+  static_assert(MODE == kResidNR || MODE == kSmoothDot, "fp32 smoothing modes");
+  constexpr int GB = G / CL, KL = K / CL;
+  constexpr int NVL = MODE == kSmoothDot ? 2 * KL : 1, NV = NVL * CL;
+  __shared__ double smem[32 * NV];
+  if (*ctl.n_active == 0) return;
+  constexpr int NPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const int bl = g / CL, cl = g % CL;
+  const int kc = cl * KL;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double part[NVL];
+#pragma unroll
+  for (int j = 0; j < NVL; ++j) part[j] = 0.0;
+  for (int64_t wn = warp * NPW; wn < A.n_nodes; wn += n_warps * NPW) {
+    const int64_t i = wn + lane / G;
+    const bool valid = i < A.n_nodes;
+    float2 acc[3][KL], accv[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_float2(0.f, 0.f);
+    int cf_i = -1;
+    if (valid) {
+      const int c32 = (int)(i >> 5);
+      const int o32 = A.e_off[c32];
+      const int w32 = (A.e_off[c32 + 1] - o32) >> 5;
+      const int sbase = o32 + (int)(i & 31), be = sbase + 32 * w32;
+      constexpr int GS = 32 * GB;
+      int q = sbase + 32 * bl;
+      int m_nx = 0;
+      float B_nx[3][3], Im_nx[3];
+      if (q < be) {
+        m_nx = ldg_i(A.blk_col + q);
+        load_block32(A, q, B_nx, Im_nx);
+      }
+      for (; q < be; q += GS) {
+        const int m = m_nx;
+        float B[3][3], Im[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          Im[c] = Im_nx[c];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) B[c][d] = B_nx[c][d];
+        }
+        if (q + GS < be) {  // software pipeline: the next block's loads in flight
+          m_nx = ldg_i(A.blk_col + q + GS);
+          load_block32(A, q + GS, B_nx, Im_nx);
+        }
+        const float2* xm = x + (int64_t)3 * m * K + kc;
+        constexpr int KP = (KL % 2 == 0) ? 2 : 1;
+#pragma unroll
+        for (int k0 = 0; k0 < KL; k0 += KP) {
+          float2 xp[3][KP];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if constexpr (KP == 2) ld2xf(xm + d * K + k0, xp[d][0], xp[d][1]);
+            else xp[d][0] = __ldg(xm + d * K + k0);
+          }
+#pragma unroll
+          for (int kk = 0; kk < KP; ++kk) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              float2 s = acc[c][k0 + kk];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                s.x = fmaf(B[c][d], xp[d][kk].x, s.x);
+                s.y = fmaf(B[c][d], xp[d][kk].y, s.y);
+              }
+              s.x = fmaf(-Im[c], xp[c][kk].y, s.x);
+              s.y = fmaf(Im[c], xp[c][kk].x, s.y);
+              acc[c][k0 + kk] = s;
+            }
+          }
+        }
+      }
+      cf_i = A.cond_fwd[i];
+      if (cf_i >= 0) {
+        const int ce = A.cpl_ptr[i + 1];
+        for (int qq = A.cpl_ptr[i] + bl; qq < ce; qq += GB) {
+          const int2 mi = ldg_i2(A.cpl_idx + qq);
+          float c0[4], c1[4];
+          ld4f(A.cpl + 4 * qq, c0);
+          ld4f(A.cpl + 4 * (A.ncpl + qq), c1);
+          const float av[3] = {c0[0], c0[1], c0[2]}, va[3] = {c0[3], c1[0], c1[1]};
+          const float2 vv = make_float2(c1[2], c1[3]);
+          const float2* xm = x + (int64_t)3 * mi.x * K + kc;
+          const float2* xvp = x + (A.na + mi.y) * K + kc;
+#pragma unroll
+          for (int k = 0; k < KL; ++k) {
+            const float2 v = __ldg(xvp + k);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              acc[c][k].x = fmaf(av[c], v.x, acc[c][k].x);
+              acc[c][k].y = fmaf(av[c], v.y, acc[c][k].y);
+            }
+            float2 s = accv[k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const float2 xa = __ldg(xm + d * K + k);
+              s.x = fmaf(va[d], xa.x, s.x);
+              s.y = fmaf(va[d], xa.y, s.y);
+            }
+            s.x += vv.x * v.x - vv.y * v.y;
+            s.y += vv.x * v.y + vv.y * v.x;
+            accv[k] = s;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+#pragma unroll
+      for (int o = (GB / 2) * CL; o >= CL; o >>= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          acc[c][k].x += __shfl_xor_sync(0xffffffffu, acc[c][k].x, o, G);
+          acc[c][k].y += __shfl_xor_sync(0xffffffffu, acc[c][k].y, o, G);
+        }
+        accv[k].x += __shfl_xor_sync(0xffffffffu, accv[k].x, o, G);
+        accv[k].y += __shfl_xor_sync(0xffffffffu, accv[k].y, o, G);
+      }
+    }
+    if (bl == 0 && valid) {
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c == 3 && cf_i < 0) break;
+          const int64_t row = c < 3 ? 3 * i + c : A.na + cf_i;
+          const float2 a32 = c < 3 ? acc[c][k] : accv[k];
+          const int64_t idx = row * K + kc + k;
+          const double2 bv = b[idx];
+          const double2 res = make_double2(bv.x - (double)a32.x, bv.y - (double)a32.y);
+          if constexpr (MODE == kResidNR) {
+            static_cast<float2*>(yv)[idx] = make_float2((float)res.x, (float)res.y);
+          } else {
+            const double2 d = ctl.dinv[row];
+            const float2 xv = x[idx];
+            const double2 z = cadd(make_double2(xv.x, xv.y),
+                                   cmul(make_double2(ctl.omega * d.x, ctl.omega * d.y), res));
+            static_cast<double2*>(yv)[idx] = z;
+            part[2 * k] += bv.x * z.x - bv.y * z.y;
+            part[2 * k + 1] += bv.x * z.y + bv.y * z.x;
+          }
+        }
+      }
+    }
+  }
+  if constexpr (MODE == kResidNR) return;
+  double bsum[NV];
+  block_sum_slots<NVL, CL>(part, smem, bsum);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) ctl.partial[(size_t)blockIdx.x * NV + j] = bsum[j];
+  if (!last_block(ctl.counter)) return;
+  double tot[NV];
+  reduce_partials<NV>(ctl.partial, tot, smem);
+  if (threadIdx.x == 0) {
+    fin_rho<K>(ctl, tot);
+    *ctl.counter = 0u;
+  }
+}
+
+template <int K, int MODE>
+const void* nbe32_fn() {
+  if constexpr (K <= 2) return (const void*)k_nbe32<2, K, MODE, 3, 1>;
+  else if constexpr (K == 4) return (const void*)k_nbe32<4, K, MODE, 3, 2>;
+  else if constexpr (K == 8) return (const void*)k_nbe32<8, K, MODE, 2, 4>;
+  else return (const void*)k_nbe32<8, K, MODE, 2, 8>;
+}
+
+__global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = (float)a[e];
+}
+
 // ---- aggregation-multigrid cycle (setup in amg.cu) ----------------------------
 // M r for the preconditioned COCG: per level l with right-hand side b_l
 //   x = omega D^-1 b                 (k_vscale)
@@ -2172,36 +2445,41 @@ namespace {
 
 __device__ __forceinline__ bool idle(const int* n_active) { return *n_active == 0; }
 
-template <int K>
+
+// x = omega D^-1 b (x fp64 or fp32)
+template <int K, typename TO>
 __global__ void __launch_bounds__(kBlock)
 k_vscale(int64_t n, const double2* __restrict__ b, const double2* __restrict__ dinv, double omega,
-         double2* __restrict__ x, const int* n_active) {
+         TO* __restrict__ x, const int* n_active) {
   if (idle(n_active)) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
        e += (int64_t)gridDim.x * blockDim.x) {
     const double2 d = dinv[e / K];
-    x[e] = cmul(make_double2(omega * d.x, omega * d.y), b[e]);
+    put(x + e, cmul(make_double2(omega * d.x, omega * d.y), b[e]));
   }
 }
 
-template <int K>
+// b_c = P^T t: fixed-order sum over the aggregate's dofs (t fp64 or fp32)
+template <int K, typename TI>
 __global__ void __launch_bounds__(kBlock)
 k_restrict(int64_t nc, const int* __restrict__ r_ptr, const int* __restrict__ r_idx,
-           const double2* __restrict__ t, double2* __restrict__ bc, const int* n_active) {
+           const TI* __restrict__ t, double2* __restrict__ bc, const int* n_active) {
   if (idle(n_active)) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nc * K;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / K, k = e - c * K;
     double2 acc = make_double2(0.0, 0.0);
-    for (int p = r_ptr[c]; p < r_ptr[c + 1]; ++p) acc = cadd(acc, t[(int64_t)r_idx[p] * K + k]);
+    for (int p = r_ptr[c]; p < r_ptr[c + 1]; ++p)
+      acc = cadd(acc, as_d2(t[(int64_t)r_idx[p] * K + k]));
     bc[e] = acc;
   }
 }
 
-template <int K>
+// x += oc P e (x fp64 or fp32)
+template <int K, typename TO>
 __global__ void __launch_bounds__(kBlock)
 k_prolong(int64_t n, const int* __restrict__ cmap, double oc, const double2* __restrict__ ec,
-          double2* __restrict__ x, const int* n_active) {
+          TO* __restrict__ x, const int* n_active) {
   if (idle(n_active)) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * K;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -2209,7 +2487,7 @@ k_prolong(int64_t n, const int* __restrict__ cmap, double oc, const double2* __r
     const int c = cmap[i];
     if (c < 0) continue;
     const double2 v = ec[(int64_t)c * K + (e - i * K)];
-    x[e] = cadd(x[e], make_double2(oc * v.x, oc * v.y));
+    put(x + e, cadd(as_d2(x[e]), make_double2(oc * v.x, oc * v.y)));
   }
 }
 
@@ -2308,8 +2586,26 @@ struct Cycle {
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx->num_sms * 8));
   }
   int grid_vec = 1;                   // <= the partial-buffer rows of the solve
+  bool f32 = false;                   // finest-level smoothing in fp32 (NB-E storage)
+  int grid32[6] = {};
   Cycle(ect_ctx* c, ect_matrix* m, Amg& h) : ctx(c), a(m), H(h) {
     grid_vec = DK::vec_grid(ctx);
+    f32 = H.f32 && a->has_nb && a->has_nbe && H.lv.size() > 1;
+    if (f32) {
+      if (!H.blk32.p) {  // fp32 copies of the NB-E blocks and couplings, once
+        H.blk32.alloc(12 * (size_t)std::max<int64_t>(1, a->nbe_slots));
+        H.cpl32.alloc(8 * (size_t)std::max<int64_t>(1, a->nb_ncpl));
+        k_to_f32<<<gvec(12 * a->nbe_slots), kBlock, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(a->nbe_blk.p), 12 * a->nbe_slots, H.blk32.p);
+        CK_LAUNCH();
+        k_to_f32<<<gvec(8 * a->nb_ncpl), kBlock, 0, ctx->stream>>>(
+            reinterpret_cast<const double*>(a->nb_cpl.p), 8 * a->nb_ncpl, H.cpl32.p);
+        CK_LAUNCH();
+        note_launch(ctx, 2);
+      }
+      grid32[kResidNR] = grid_for(ctx, nbe32_fn<K, kResidNR>(), kBlock);
+      grid32[kSmoothDot] = grid_for(ctx, nbe32_fn<K, kSmoothDot>(), kBlock);
+    }
     for (int mode : {kResidNR, kSmooth, kSmoothDot}) grid0[mode] = DK::spmv_grid(ctx, mode, a);
     gl.resize(H.lv.size());
     constexpr int G = csr_lanes<K>();
@@ -2326,6 +2622,10 @@ struct Cycle {
         L.xt.alloc((size_t)L.n * K);
         if (l > 0) L.t.alloc((size_t)L.n * K);
       }
+      if (H.f32 && H.lv.size() > 1) {
+        H.xt32.alloc((size_t)H.lv[0].n * K);
+        H.t32.alloc((size_t)H.lv[0].n * K);
+      }
       for (size_t l = 1; l < H.lv.size(); ++l) {
         AmgLevel& L = H.lv[l];
         for (auto* v : {&L.b, &L.out, &L.b2, &L.out2}) v->alloc((size_t)L.n * K);
@@ -2333,7 +2633,49 @@ struct Cycle {
       H.kcap = K;
     }
   }
-  int max_grid() const { return std::max({grid0[kResidNR], grid0[kSmooth], grid0[kSmoothDot]}); }
+  int max_grid() const {
+    return std::max({grid0[kResidNR], grid0[kSmooth], grid0[kSmoothDot], grid32[kSmoothDot]});
+  }
+  Nb32 nb32() const {
+    return Nb32{a->nbe_off.p, a->nbe_col.p, H.blk32.p, a->nbe_slots, a->nb_cpl_ptr.p,
+                a->nb_cpl_idx.p, H.cpl32.p, a->nb_ncpl, a->nb_cond_fwd, a->n_nodes,
+                3 * a->n_nodes};
+  }
+  void spmv32(int mode, const float2* x, void* y, const double2* b, KrylovCtl c) {
+    c.dinv = a->dinv.p;
+    Nb32 v = nb32();
+    void* args[] = {&v, (void*)&x, &y, (void*)&b, &c};
+    const void* fn = mode == kResidNR ? nbe32_fn<K, kResidNR>() : nbe32_fn<K, kSmoothDot>();
+    CK(cudaLaunchKernel(fn, dim3(grid32[mode]), dim3(kBlock), args, 0, ctx->stream));
+  }
+  // finest level with fp32 smoothing: b = r (fp64), out = z (fp64), dot always
+  void run0_f32(const double2* b, double2* out, KrylovCtl c, bool pre) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = H.lv[0].n;
+    const int* na = c.n_active;
+    c.omega = H.omega;
+    if (!pre) {
+      k_vscale<K, float2><<<gvec(n * K), kBlock, 0, s>>>(n, b, a->dinv.p, H.omega, H.xt32.p, na);
+      CK_LAUNCH();
+    }
+    spmv32(kResidNR, H.xt32.p, H.t32.p, b, c);
+    AmgLevel& L = H.lv[0];
+    AmgLevel& C = H.lv[1];
+    k_restrict<K, float2><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, L.r_ptr.p, L.r_idx.p, H.t32.p,
+                                                           C.b.p, na);
+    CK_LAUNCH();
+    run(1, C.b.p, C.out.p, nullptr, c, false);
+    if (H.wcycle && H.lv.size() > 2) {
+      spmv(1, kResidNR, C.out.p, C.b2.p, C.b.p, c);
+      run(1, C.b2.p, C.out2.p, nullptr, c, false);
+      k_axpy1<K><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, C.out.p, C.out2.p, na);
+      CK_LAUNCH();
+    }
+    k_prolong<K, float2><<<gvec(n * K), kBlock, 0, s>>>(n, L.cmap.p, H.oc, C.out.p, H.xt32.p, na);
+    CK_LAUNCH();
+    spmv32(kSmoothDot, H.xt32.p, out, b, c);
+    note_launch(ctx, 6);
+  }
   void spmv(size_t l, int mode, const double2* x, double2* y, const double2* b, KrylovCtl c) {
     if (l == 0) {
       c.dinv = a->dinv.p;
@@ -2348,6 +2690,10 @@ struct Cycle {
   // x = omega D^-1 b is already in xt (fused into the COCG update)
   void run(size_t l, const double2* b, double2* out, double2* t0, KrylovCtl c, bool dot,
            bool pre = false) {
+    if (l == 0 && f32 && dot) {
+      run0_f32(b, out, c, pre);
+      return;
+    }
     cudaStream_t s = ctx->stream;
     AmgLevel& L = H.lv[l];
     const int64_t n = L.n;
@@ -2370,12 +2716,13 @@ struct Cycle {
     double2* xt = L.xt.p;
     double2* t = l == 0 ? t0 : L.t.p;
     if (!pre) {
-      k_vscale<K><<<gvec(n * K), kBlock, 0, s>>>(n, b, dinv, H.omega, xt, na);
+      k_vscale<K, double2><<<gvec(n * K), kBlock, 0, s>>>(n, b, dinv, H.omega, xt, na);
       CK_LAUNCH();
     }
     spmv(l, kResidNR, xt, t, b, c);
     AmgLevel& C = H.lv[l + 1];
-    k_restrict<K><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, L.r_ptr.p, L.r_idx.p, t, C.b.p, na);
+    k_restrict<K, double2><<<gvec(C.n * K), kBlock, 0, s>>>(C.n, L.r_ptr.p, L.r_idx.p, t, C.b.p,
+                                                            na);
     CK_LAUNCH();
     run(l + 1, C.b.p, C.out.p, t0, c, false);
     if (H.wcycle && l + 2 < H.lv.size()) {
@@ -2385,7 +2732,7 @@ struct Cycle {
       CK_LAUNCH();
       note_launch(ctx, 2);
     }
-    k_prolong<K><<<gvec(n * K), kBlock, 0, s>>>(n, L.cmap.p, H.oc, C.out.p, xt, na);
+    k_prolong<K, double2><<<gvec(n * K), kBlock, 0, s>>>(n, L.cmap.p, H.oc, C.out.p, xt, na);
     CK_LAUNCH();
     spmv(l, dot ? kSmoothDot : kSmooth, xt, out, b, c);
     note_launch(ctx, 5);
@@ -2515,7 +2862,8 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
           if (ext) {
             const bool fuse = a->amg->lv.size() > 1;
             k_update<KW, true><<<grid_v, kBlock, 0, s>>>(
-                n, r.p, q.p, a->dinv.p, ctl, fuse ? a->amg->lv[0].xt.p : nullptr, a->amg->omega);
+                n, r.p, q.p, a->dinv.p, ctl, fuse && !cyc->f32 ? a->amg->lv[0].xt.p : nullptr,
+                a->amg->omega, fuse && cyc->f32 ? a->amg->xt32.p : nullptr);
             CK_LAUNCH();
             prof_end(ctx, ev2);
             cudaEvent_t ev3[2];
@@ -2615,13 +2963,6 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
 // the partitioned path is validated on a single GPU.
 namespace {
 
-__global__ void k_scatter_cols(const int* __restrict__ idx, int64_t n, const int* __restrict__ map,
-                               int* out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = map[idx[i]];
-}
-
 template <int K>
 __global__ void k_pack(const double2* __restrict__ v, const int* __restrict__ nodes, int64_t ns,
                        const int* __restrict__ cnodes, int64_t nsc,
@@ -2647,7 +2988,7 @@ __global__ void k_sum_parts(double* const* reds, int n_parts, int nv) {
 }
 
 NbView part_view(const ect_part* P) {
-  NbView v{P->blk_ptr.p, P->blk_col.p, reinterpret_cast<const double*>(P->blk.p), P->nblk,
+  NbView v{P->blk_ptr.p, P->nbe_col.p, reinterpret_cast<const double*>(P->nbe_blk.p), P->nbe_slots,
            P->cpl_ptr.p, P->cpl_idx.p, reinterpret_cast<const double*>(P->cpl.p), P->ncpl,
            P->cond_local.p, P->plan.L, P->plan.na_local()};
   if (P->has_nbe) {  // sliced-ELL copy of the part's blocks (the default SpMV layout)
@@ -2714,7 +3055,7 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
     P->int_lo = best_lo;
     P->int_hi = best_lo + best_len;
   }
-  // blocks of the owned nodes: contiguous slice of the global NB arrays
+  // block pointers of the owned nodes (their NB-E slots come from the global NB-E below)
   const int64_t q0 = nbr_off[H.n0], q1 = nbr_off[H.n1];
   P->nblk = q1 - q0;
   P->blk_ptr.alloc(L + 1);
@@ -2722,17 +3063,6 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
     std::vector<int> bp(L + 1);
     for (int64_t i = 0; i <= L; ++i) bp[i] = nbr_off[H.n0 + i] - (int)q0;
     CK(cudaMemcpy(P->blk_ptr.p, bp.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice));
-  }
-  P->blk_col.alloc(std::max<int64_t>(1, P->nblk));
-  P->blk.alloc(6 * std::max<int64_t>(1, P->nblk));
-  if (P->nblk) {
-    k_scatter_cols<<<(int)std::min<int64_t>((P->nblk + 255) / 256, ctx->num_sms * 16), 256, 0, s>>>(
-        m->nbr.p + q0, P->nblk, d_g2l.p, P->blk_col.p);
-    CK_LAUNCH();
-    for (int pl = 0; pl < 3; ++pl)
-      CK(cudaMemcpyAsync(reinterpret_cast<double*>(P->blk.p) + 4 * pl * P->nblk,
-                         reinterpret_cast<const double*>(a->nb_blk.p) + 4 * (pl * a->nb_blocks + q0),
-                         4 * P->nblk * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   // couplings of the owned nodes
   const int64_t c0 = cpl_ptr[H.n0], c1 = cpl_ptr[H.n1];
@@ -2795,11 +3125,12 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
     CK(cudaStreamSynchronize(s));
     P->nbe_col.alloc(std::max(1, slots));
     P->nbe_blk.alloc(6 * (size_t)std::max(1, slots));
+    if (!a->has_nbe) fail(ECT_ERR_SOLVER, "part: the global matrix has no NB-E blocks");
     const int fg = (int)std::min<int64_t>((32 * nch + 255) / 256, (int64_t)ctx->num_sms * 16);
-    k_nbe_fill<<<std::max(fg, 1), 256, 0, s>>>(P->blk_ptr.p, P->blk_col.p,
-                                                reinterpret_cast<const double*>(P->blk.p), P->nblk,
-                                                L, nch, P->nbe_off.p, P->nbe_col.p,
-                                                reinterpret_cast<double*>(P->nbe_blk.p), slots);
+    k_part_nbe_fill<<<std::max(fg, 1), 256, 0, s>>>(
+        P->blk_ptr.p, L, H.n0, a->nbe_off.p, a->nbe_col.p,
+        reinterpret_cast<const double*>(a->nbe_blk.p), a->nbe_slots, d_g2l.p, P->nbe_off.p, nch,
+        P->nbe_col.p, reinterpret_cast<double*>(P->nbe_blk.p), slots);
     CK_LAUNCH();
     P->nbe_slots = slots;
     P->has_nbe = true;
@@ -2807,6 +3138,174 @@ ect_part* create_part(ect_mesh* m, ect_matrix* a, const int64_t* splits, int n_p
   }
   CK(cudaStreamSynchronize(s));
   note_launch(ctx, 1);
+  return P.release();
+}
+
+// The part of `create_part` built without a global matrix: the slab's rows
+// are patterned and assembled on their own (build_pattern / assemble_values
+// over nodes [n0, n1), global indices, the other rows empty), the slab's NB
+// blocks cut from that CSR, then the same local renumbering, halo plan and
+// NB-E layout. Device memory per rank ~ the slab's share of the matrix, as the
+// reference's per-partition assembly (assembly.cpp:246-258) and the paper's
+// per-rank matrices.
+ect_part* create_part_assembled(ect_mesh* m, const ect_materials& mats, const int64_t* splits,
+                                int n_parts, int part) {
+  ect_ctx* ctx = m->ctx;
+  cudaStream_t s = ctx->stream;
+  if (mats.ibc_enabled) fail(ECT_ERR_SOLVER, "part: impedance surface terms are not partitioned");
+  const int64_t nn = m->n_nodes;
+  if (!m->have_nbr) {  // the mesh-level neighbour lists (K1) are shared by every slab
+    ect_matrix probe;
+    probe.ctx = ctx;
+    build_pattern(m, &probe, 0, 0);
+  }
+  std::vector<int> nbr_off(nn + 1), cond(nn);
+  CK(cudaMemcpyAsync(nbr_off.data(), m->nbr_off.p, (nn + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(cond.data(), m->cond_fwd.p, nn * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<int> nbr(nbr_off[nn]);
+  CK(cudaMemcpy(nbr.data(), m->nbr.p, nbr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  auto P = std::make_unique<ect_part>();
+  P->ctx = ctx;
+  P->plan = build_halo_plan(nn, nbr_off.data(), nbr.data(), cond.data(), splits, n_parts, part);
+  const HaloPlan& H = P->plan;
+  P->n_nodes_global = nn;
+  P->na_global = 3 * nn;
+  P->n_global = 3 * nn + m->n_cond;
+  const int64_t L = H.L, G = H.G, NL = H.n_local();
+  std::vector<int> g2l(nn, -1);
+  for (int64_t i = 0; i < L; ++i) g2l[H.n0 + i] = (int)i;
+  for (int64_t q = 0; q < G; ++q) g2l[H.ghost_nodes[q]] = (int)(L + q);
+  DevBuf<int> d_g2l(nn);
+  CK(cudaMemcpy(d_g2l.p, g2l.data(), nn * sizeof(int), cudaMemcpyHostToDevice));
+  {
+    int64_t best_lo = 0, best_len = 0, run_lo = 0;
+    for (int64_t i = 0; i <= L; ++i) {
+      bool boundary = i == L;
+      if (i < L)
+        for (int q = nbr_off[H.n0 + i]; q < nbr_off[H.n0 + i + 1] && !boundary; ++q)
+          boundary = g2l[nbr[q]] >= L;
+      if (boundary) {
+        if (i - run_lo > best_len) {
+          best_len = i - run_lo;
+          best_lo = run_lo;
+        }
+        run_lo = i + 1;
+      }
+    }
+    P->int_lo = best_lo;
+    P->int_hi = best_lo + best_len;
+  }
+  // ---- the slab's rows, patterned and assembled alone ----------------------
+  ect_matrix slab;
+  slab.ctx = ctx;
+  build_pattern(m, &slab, H.n0, H.n1);
+  assemble_values(m, mats, &slab);
+  // ---- its NB blocks (owned nodes only) ------------------------------------
+  const int64_t q0 = nbr_off[H.n0], q1 = nbr_off[H.n1];
+  P->nblk = q1 - q0;
+  DevBuf<int> cnt(nn + 1), cpl_ptr(nn + 1);
+  CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), s));
+  const int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>((L + 255) / 256, ctx->num_sms * 16));
+  k_cpl_count<<<cgrid, 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p, m->cond_fwd.p, H.n0, H.n1, cnt.p);
+  CK_LAUNCH();
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.p, cpl_ptr.p, nn + 1, s));
+  CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, cnt.p, cpl_ptr.p, nn + 1, s));
+  std::vector<int> h_cpl(nn + 1);
+  CK(cudaMemcpyAsync(h_cpl.data(), cpl_ptr.p, (nn + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t c0 = h_cpl[H.n0];  // = 0: only owned nodes were counted
+  P->ncpl = h_cpl[H.n1] - c0;
+  DevBuf<double2> blk(6 * std::max<int64_t>(1, P->nblk));
+  DevBuf<int2> cidx(std::max<int64_t>(1, P->ncpl));
+  P->cpl.alloc(4 * std::max<int64_t>(1, P->ncpl));
+  DevBuf<int> bad(1);
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((32 * L + 255) / 256, ctx->num_sms * 16));
+  k_build_nb<<<wgrid, 256, 0, s>>>(slab.row_ptr.p, slab.val.p, m->nbr_off.p, m->nbr.p,
+                                   m->nbr_cond.p, m->cond_fwd.p, cpl_ptr.p, nn,
+                                   reinterpret_cast<double*>(blk.p), P->nblk, cidx.p,
+                                   reinterpret_cast<double*>(P->cpl.p), P->ncpl, bad.p, H.n0, H.n1,
+                                   q0, c0);
+  CK_LAUNCH();
+  int h_bad = 0;
+  CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h_bad) fail(ECT_ERR_SOLVER, "part: node blocks carry imaginary off-diagonal parts");
+  // local node-block structure
+  P->blk_ptr.alloc(L + 1);
+  P->cpl_ptr.alloc(L + 1);
+  {
+    std::vector<int> bp(L + 1), cp(L + 1);
+    for (int64_t i = 0; i <= L; ++i) {
+      bp[i] = nbr_off[H.n0 + i] - (int)q0;
+      cp[i] = h_cpl[H.n0 + i] - (int)c0;
+    }
+    CK(cudaMemcpy(P->blk_ptr.p, bp.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(P->cpl_ptr.p, cp.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  DevBuf<int> lcol(std::max<int64_t>(1, P->nblk));
+  {
+    std::vector<int> lc(P->nblk);
+    for (int64_t q = q0; q < q1; ++q) lc[q - q0] = g2l[nbr[q]];
+    if (P->nblk) CK(cudaMemcpy(lcol.p, lc.data(), P->nblk * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  P->cpl_idx.alloc(std::max<int64_t>(1, P->ncpl));
+  if (P->ncpl) {
+    std::vector<int2> ci(P->ncpl);
+    CK(cudaMemcpy(ci.data(), cidx.p, P->ncpl * sizeof(int2), cudaMemcpyDeviceToHost));
+    for (auto& e : ci) {
+      const int l = g2l[e.x];
+      e = make_int2(l, H.local_vdof[l]);
+    }
+    CK(cudaMemcpy(P->cpl_idx.p, ci.data(), P->ncpl * sizeof(int2), cudaMemcpyHostToDevice));
+  }
+  P->cond_local.alloc(std::max<int64_t>(1, L + G));
+  CK(cudaMemcpy(P->cond_local.p, H.local_vdof.data(), (L + G) * sizeof(int), cudaMemcpyHostToDevice));
+  P->dinv.alloc(NL);
+  CK(cudaMemsetAsync(P->dinv.p, 0, P->dinv.bytes(), s));
+  CK(cudaMemcpyAsync(P->dinv.p, slab.dinv.p + 3 * H.n0, 3 * L * sizeof(double2),
+                     cudaMemcpyDeviceToDevice, s));
+  if (H.Vo)
+    CK(cudaMemcpyAsync(P->dinv.p + H.na_local(), slab.dinv.p + 3 * nn + H.c0,
+                       H.Vo * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  for (const auto& peer : H.peers) {
+    ect_part::Peer d;
+    d.ns = (int64_t)peer.send_nodes.size();
+    d.nsc = (int64_t)peer.send_cond_nodes.size();
+    d.send_nodes.alloc(std::max<int64_t>(1, d.ns));
+    d.send_cond.alloc(std::max<int64_t>(1, d.nsc));
+    if (d.ns) CK(cudaMemcpy(d.send_nodes.p, peer.send_nodes.data(), d.ns * sizeof(int), cudaMemcpyHostToDevice));
+    if (d.nsc) CK(cudaMemcpy(d.send_cond.p, peer.send_cond_nodes.data(), d.nsc * sizeof(int), cudaMemcpyHostToDevice));
+    P->peers.push_back(std::move(d));
+  }
+  // NB-E layout of the part
+  {
+    const int64_t nch = (L + 31) / 32;
+    DevBuf<int> w(nch + 1);
+    const int cg = (int)std::min<int64_t>((nch + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_nbe_width<<<std::max(cg, 1), 256, 0, s>>>(P->blk_ptr.p, L, nch, w.p);
+    CK_LAUNCH();
+    P->nbe_off.alloc(nch + 1);
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, w.p, P->nbe_off.p, nch + 1, s));
+    CK(cub::DeviceScan::ExclusiveSum(cub_scratch(ctx, tmp), tmp, w.p, P->nbe_off.p, nch + 1, s));
+    int slots = 0;
+    CK(cudaMemcpyAsync(&slots, P->nbe_off.p + nch, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    P->nbe_col.alloc(std::max(1, slots));
+    P->nbe_blk.alloc(6 * (size_t)std::max(1, slots));
+    const int fg = (int)std::min<int64_t>((32 * nch + 255) / 256, (int64_t)ctx->num_sms * 16);
+    k_nbe_fill<<<std::max(fg, 1), 256, 0, s>>>(P->blk_ptr.p, lcol.p,
+                                                reinterpret_cast<const double*>(blk.p), P->nblk,
+                                                L, nch, P->nbe_off.p, P->nbe_col.p,
+                                                reinterpret_cast<double*>(P->nbe_blk.p), slots);
+    CK_LAUNCH();
+    P->nbe_slots = slots;
+    P->has_nbe = true;
+  }
+  note_launch(ctx, 6);
+  CK(cudaStreamSynchronize(s));
   return P.release();
 }
 

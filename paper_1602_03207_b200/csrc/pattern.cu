@@ -70,9 +70,10 @@ __global__ void k_count_neighbours(const int* __restrict__ inc_off, const int* _
 
 // Row lengths: A-rows 3u + cc, V-row 4 cc (u neighbours, cc via conductor tets).
 __global__ void k_row_lengths(const int* __restrict__ nbr_off, const uint8_t* __restrict__ nbr_cond,
-                              const int* __restrict__ cond_fwd, int64_t n_nodes, int* row_len) {
+                              const int* __restrict__ cond_fwd, int64_t n_nodes, int* row_len,
+                              int64_t lo, int64_t hi) {
   const int64_t na = 3 * n_nodes;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_nodes;
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int b = nbr_off[i], u = nbr_off[i + 1] - b;
     int cc = 0;
@@ -115,12 +116,12 @@ __global__ void k_narrow_row_ptr(const long long* __restrict__ in, int64_t n, in
 __global__ void k_fill_columns(const int* __restrict__ nbr_off, const int* __restrict__ nbr,
                                const uint8_t* __restrict__ nbr_cond,
                                const int* __restrict__ cond_fwd, const int* __restrict__ row_ptr,
-                               int64_t n_nodes, int* col) {
+                               int64_t n_nodes, int* col, int64_t lo, int64_t hi) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int na = (int)(3 * n_nodes);
-  for (int64_t i = warp; i < n_nodes; i += n_warps) {
+  for (int64_t i = lo + warp; i < hi; i += n_warps) {
     const int b = nbr_off[i], u = nbr_off[i + 1] - b;
     // total conductor neighbours
     int cc = 0;
@@ -400,16 +401,21 @@ static void build_neighbours(ect_mesh* m) {
   m->max_nbr = max_nbr;
 }
 
-void build_pattern(ect_mesh* m, ect_matrix* a) {
+void build_pattern(ect_mesh* m, ect_matrix* a, int64_t lo, int64_t hi) {
   ect_ctx* ctx = m->ctx;
   cudaStream_t s = ctx->stream;
   if (!m->have_nbr) build_neighbours(m);
   const int64_t nn = m->n_nodes;
+  if (hi < 0) hi = nn;
+  // rows of nodes [lo, hi) only (a slab of a row partition): the other rows
+  // stay empty, indices stay global
+  a->node_lo = lo;
+  a->node_hi = hi;
   const int64_t N = 3 * nn + m->n_cond;
   DevBuf<int> row_len(N + 1);
   CK(cudaMemsetAsync(row_len.p, 0, row_len.bytes(), s));
-  k_row_lengths<<<blocks_for(ctx, nn), 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p, m->cond_fwd.p,
-                                                   nn, row_len.p);
+  k_row_lengths<<<blocks_for(ctx, hi - lo), 256, 0, s>>>(m->nbr_off.p, m->nbr_cond.p,
+                                                        m->cond_fwd.p, nn, row_len.p, lo, hi);
   CK_LAUNCH();
   size_t tmp = 0;
   DevBuf<long long> rp64(N + 1);
@@ -431,9 +437,8 @@ void build_pattern(ect_mesh* m, ect_matrix* a) {
   a->val.alloc(std::max<long long>(1, nnz));
   k_narrow_row_ptr<<<blocks_for(ctx, N + 1), 256, 0, s>>>(rp64.p, N + 1, a->row_ptr.p);
   CK_LAUNCH();
-  k_fill_columns<<<blocks_for(ctx, 32 * nn), 256, 0, s>>>(m->nbr_off.p, m->nbr.p, m->nbr_cond.p,
-                                                         m->cond_fwd.p, a->row_ptr.p, nn,
-                                                         a->col.p);
+  k_fill_columns<<<blocks_for(ctx, 32 * (hi - lo)), 256, 0, s>>>(
+      m->nbr_off.p, m->nbr.p, m->nbr_cond.p, m->cond_fwd.p, a->row_ptr.p, nn, a->col.p, lo, hi);
   CK_LAUNCH();
   note_launch(ctx, 4);
   CK(cudaStreamSynchronize(s));

@@ -540,13 +540,19 @@ class Comm:
 
 
 class Part:
-    """Rows of nodes [splits[part], splits[part+1]) of an assembled matrix."""
+    """Rows of nodes [splits[part], splits[part+1]) of an assembled matrix, or
+    (matrix=None, mats=MaterialTable) assembled slab-locally without one."""
 
-    def __init__(self, ctx: Context, mesh: Mesh, matrix: Matrix, splits, part: int):
+    def __init__(self, ctx: Context, mesh: Mesh, matrix: Matrix | None, splits, part: int,
+                 mats: Materials | None = None):
         splits = np.ascontiguousarray(splits, np.int64)
         h = VP()
-        _check(lib().ect_part_create(ctx.h, mesh.h, matrix.h, _ptr(splits), I32(len(splits) - 1),
-                                     I32(part), C.byref(h)))
+        if matrix is None:
+            _check(lib().ect_part_create_assembled(ctx.h, mesh.h, C.byref(mats), _ptr(splits),
+                                                   I32(len(splits) - 1), I32(part), C.byref(h)))
+        else:
+            _check(lib().ect_part_create(ctx.h, mesh.h, matrix.h, _ptr(splits),
+                                         I32(len(splits) - 1), I32(part), C.byref(h)))
         self.h, self.ctx = h, ctx
         info = (I64 * 8)()
         _check(lib().ect_part_info(h, info))

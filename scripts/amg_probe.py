@@ -17,7 +17,7 @@ from paper_1602_03207_b200 import workloads
 from paper_1602_03207_b200.workloads import Workload, _coil
 
 
-def cocg(A, b, apply_m, tol=1e-8, max_iter=int(__import__("os").environ.get("MAXIT", 5000))):
+def cocg(A, b, apply_m, tol=float(__import__("os").environ.get("TOL", 1e-8)), max_iter=int(__import__("os").environ.get("MAXIT", 5000))):
     x = np.zeros_like(b)
     r = b.copy()
     z = apply_m(r)
@@ -139,11 +139,28 @@ def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=int(__import__("os
     return levels
 
 
+F32 = __import__("os").environ.get("F32") == "1"
+
+
 def vcycle(levels, b, lvl=0, nu=1, w=0.7, gamma=1, oc=1.0):
     L = levels[lvl]
     if "lu" in L:
         return L["lu"].solve(b)
     A, P, d = L["A"], L["P"], L["d"]
+    if F32 and lvl == 0:  # finest level smoothing in single precision
+        if "A32" not in L:
+            L["A32"] = A.astype(np.complex64)
+        A32 = L["A32"]
+        b32 = b.astype(np.complex64)
+        x = (w * b / d).astype(np.complex64)
+        r = (b32 - A32 @ x)
+        rc = (P.T @ r.astype(np.complex128))
+        e = vcycle(levels, rc, lvl + 1, nu, w, gamma, oc)
+        if gamma == 2 and "lu" not in levels[lvl + 1]:
+            Ac = levels[lvl + 1]["A"]
+            e = e + vcycle(levels, rc - Ac @ e, lvl + 1, nu, w, gamma, oc)
+        x = x + (oc * (P @ e)).astype(np.complex64)
+        return x.astype(np.complex128) + w * (b - (A32 @ x).astype(np.complex128)) / d
     x = w * b / d
     for _ in range(nu - 1):
         x = x + w * (b - A @ x) / d

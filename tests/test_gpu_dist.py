@@ -38,6 +38,23 @@ def test_partitioned_solve_matches_single(ctx, splits):
         assert ea <= 1e-6 and ev <= 1e-6, (ea, ev)
 
 
+@pytest.mark.parametrize("splits", [[0, 300, 637], [0, 150, 330, 500, 637]])
+def test_slab_assembled_parts_equal_cut_parts(ctx, splits):
+    """ect_part_create_assembled (only the slab's rows assembled) gives the same
+    part as cutting the assembled global matrix: bitwise-equal solves."""
+    g = golden("small_6x6x12")
+    m, a = _setup(ctx, g)
+    p, _, _ = m.materials(workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0))
+    cut = [ect.Part(ctx, m, a, splits, r) for r in range(len(splits) - 1)]
+    own = [ect.Part(ctx, m, None, splits, r, mats=p) for r in range(len(splits) - 1)]
+    assert [c.info for c in cut] == [o.info for o in own]
+    b = np.ascontiguousarray(g["rhs"].T)
+    x1, r1 = ect.dist_solve(cut, b, tol=1e-10, max_iter=20000)
+    x2, r2 = ect.dist_solve(own, b, tol=1e-10, max_iter=20000)
+    assert x1.tobytes() == x2.tobytes()
+    assert [r["iterations"] for r in r1] == [r["iterations"] for r in r2]
+
+
 def test_partitioned_configs0_vs_reference(ctx):
     w = workloads.config0()
     mm = w.mesh()

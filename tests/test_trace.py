@@ -54,23 +54,27 @@ def test_gpu_sweep_trace_matches_reference(ctx, tmp_path):
 @pytest.mark.slow
 def test_gpu_configs3_sweep_matches_reference_trace(ctx, tmp_path):
     """BASELINE configs[3] at full size: sweep positions on the configs[1] mesh
-    (4 per matrix pass, tol 1e-9) against the reference's own run_scan chain at
-    the same positions (tests/golden/trace_cfg3.csv: 4 of the 64 around the
-    deposit; GMRES(80)+ILU(0) at 1e-9; oracle/make_golden.py cfg3_trace). Bar
-    per signal over the curve: max_z |S(z) - S*(z)| / max_z |S*(z)| <= 1e-6
-    (SURVEY §8(c) impedance metric); the per-point max_relative_deviation of
-    the reference's trace diff is reported beside it."""
+    (4 per matrix pass) against the reference's own run_scan chain at the same
+    positions (tests/golden/trace_cfg3.csv: 8 of the 64 -- both far-field
+    ends, both deposit edges, the centre and three fill positions -- solved by
+    the reference's GMRES+ILU(0) to tol 1e-10 and accepted on the true
+    residual; oracle/make_golden.py cfg3_trace_batched). The GPU solves to
+    1e-12 so the bar is not spent on our own convergence error. Bar per
+    signal over the curve: max_z |S(z) - S*(z)| / max_z |S*(z)| <= 1e-6
+    (SURVEY §8(c) impedance metric); the reference's per-point
+    max_relative_deviation (scan.cpp:252-272) is reported beside it."""
     gold_path = GOLDEN / "trace_cfg3.csv"
     if not gold_path.exists():
-        pytest.skip("trace_cfg3.csv not generated (python -m oracle.make_golden cfg3_trace)")
+        pytest.skip("trace_cfg3.csv not generated (python -m oracle.make_golden cfg3_trace_batched)")
     w = workloads.config3()
     gold = trace.read_trace_csv(gold_path)
+    assert len(gold) >= 8
     # the trace stores z with 12 digits: solve at the exact sweep positions
     zs = [min(w.positions, key=lambda p, z=r[0]: abs(p - z)) for r in gold]
-    assert all(abs(z - r[0]) <= 1e-11 * abs(z) for z, r in zip(zs, gold))
+    assert all(abs(z - r[0]) <= 1e-11 * max(abs(z), 1e-12) for z, r in zip(zs, gold))
     mm = w.mesh()
     m = ect.Mesh(ctx, mm.xyz, mm.tets, mm.region)
-    s = ect.Session(ctx, m, w.physics, w.coil, w.amplitude, tol=1e-9, max_iter=200000)
+    s = ect.Session(ctx, m, w.physics, w.coil, w.amplitude, tol=1e-12, max_iter=200000)
     pts = s.solve_positions(zs, positions_per_batch=4)
     assert not any(p["failed"] for p in pts)
     out = tmp_path / "gpu_cfg3.csv"
