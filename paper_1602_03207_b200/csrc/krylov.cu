@@ -156,9 +156,15 @@ __device__ __forceinline__ void reduce_partials(const double* partial, double (&
 //  kSmooth   : y = x + omega D^-1 (b - A x) (damped-Jacobi sweep, no reduction)
 //  kSmoothDot: kSmooth, plus per column b^T y (unconjugated) -> rho = r^T z of
 //              the preconditioned COCG (b = r, y = z = M r on the finest level)
-enum Mode { kPlain = 0, kCocg = 1, kResid = 2, kResidNR = 3, kSmooth = 4, kSmoothDot = 5 };
+//  kCgDot    : y = w = A z (x = z, b = r); per column r^T z, w^T z, ||r||^2 (the
+//              single reduction of the Chronopoulos-Gear COCG, distributed solve)
+enum Mode { kPlain = 0, kCocg = 1, kResid = 2, kResidNR = 3, kSmooth = 4, kSmoothDot = 5,
+            kCgDot = 6 };
 __host__ __device__ constexpr int mode_nv(int mode, int k) {
-  return mode == kCocg || mode == kSmoothDot ? 2 * k : mode == kResid ? k : 0;
+  return mode == kCocg || mode == kSmoothDot ? 2 * k
+         : mode == kResid                    ? k
+         : mode == kCgDot                    ? 5 * k
+                                             : 0;
 }
 
 struct KrylovCtl {
@@ -328,19 +334,79 @@ __device__ void fin_start(const KrylovCtl& ctl, const double* tot, unsigned mask
   *ctl.n_active = active;
 }
 
-enum Fin { kFinAlpha = 0, kFinUpdate = 1, kFinStart = 2, kFinResid = 3 };
+// Chronopoulos-Gear COCG (one reduction per iteration): tot per column =
+// (r^T z re, im, w^T z re, im, ||r||^2) after the step r -= alpha s.
+template <int K>
+__device__ void fin_cg(const KrylovCtl& ctl, const double* tot, unsigned mask, int start,
+                       int fresh) {
+  int active = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    RhsState& s = ctl.st[k];
+    const double2 g = make_double2(tot[5 * k], tot[5 * k + 1]);
+    const double2 d = make_double2(tot[5 * k + 2], tot[5 * k + 3]);
+    const double rn = sqrt(tot[5 * k + 4]);
+    if (start) {
+      if (!((mask >> k) & 1u)) {
+        active += s.status == kActive;
+        continue;
+      }
+      if (fresh) {
+        s.bnorm = rn;  // r = b
+        s.iters = 0;
+      }
+      s.rnorm = rn;
+      s.beta = make_double2(0.0, 0.0);
+      if (fresh && s.bnorm == 0.0) s.status = kZeroRhs;
+      else if (rn <= ctl.tol * s.bnorm) s.status = kConverged;
+      else if ((g.x == 0.0 && g.y == 0.0) || (d.x == 0.0 && d.y == 0.0)) s.status = kBreakdown;
+      else {
+        s.status = kActive;
+        s.rho = g;
+        s.alpha = cdiv(g, d);
+        ++active;
+      }
+      continue;
+    }
+    if (s.status != kActive) continue;
+    s.rnorm = rn;
+    s.iters += 1;
+    if (rn <= ctl.tol * s.bnorm) {
+      s.status = kConverged;
+    } else if (s.iters >= ctl.max_iter) {
+      s.status = kMaxIter;
+    } else {
+      const double2 beta = cdiv(g, s.rho);
+      const double2 den = csub(d, cdiv(cmul(beta, g), s.alpha));
+      if ((g.x == 0.0 && g.y == 0.0) || (den.x == 0.0 && den.y == 0.0)) {
+        s.status = kBreakdown;
+      } else {
+        s.beta = beta;
+        s.alpha = cdiv(g, den);
+        s.rho = g;
+        ++active;
+      }
+    }
+  }
+  *ctl.n_active = active;
+}
+
+enum Fin { kFinAlpha = 0, kFinUpdate = 1, kFinStart = 2, kFinResid = 3, kFinCg = 4,
+           kFinCgStart = 5 };
 
 // Finalisation after a cross-part reduction of ctl.red (distributed solve).
 template <int K, int WHAT>
 __global__ void k_fin(KrylovCtl ctl, unsigned mask, int fresh) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   constexpr int NV = WHAT == kFinAlpha ? 2 * K : WHAT == kFinUpdate ? 3 * K
-                     : WHAT == kFinStart ? 4 * K : K;
-  if (WHAT != kFinStart && WHAT != kFinResid && *ctl.n_active == 0) return;
+                     : WHAT == kFinStart ? 4 * K : (WHAT == kFinCg || WHAT == kFinCgStart) ? 5 * K
+                     : K;
+  if (WHAT != kFinStart && WHAT != kFinResid && WHAT != kFinCgStart && *ctl.n_active == 0) return;
   double tot[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) tot[j] = ctl.red[j];
-  if (WHAT == kFinAlpha) fin_alpha<K>(ctl, tot);
+  if (WHAT == kFinCg || WHAT == kFinCgStart) fin_cg<K>(ctl, tot, mask, WHAT == kFinCgStart, fresh);
+  else if (WHAT == kFinAlpha) fin_alpha<K>(ctl, tot);
   else if (WHAT == kFinUpdate) fin_update<K>(ctl, tot);
   else if (WHAT == kFinStart) fin_start<K>(ctl, tot, mask, fresh);
   else fin_resid<K>(ctl, tot);
@@ -1021,6 +1087,14 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
             part[k] += rv.x * rv.x + rv.y * rv.y;
           } else if (MODE == kResidNR) {
             y[idx] = csub(b[idx], v);
+          } else if (MODE == kCgDot) {
+            y[idx] = v;
+            const double2 zz = x[idx], rr = b[idx];
+            part[5 * k] += rr.x * zz.x - rr.y * zz.y;
+            part[5 * k + 1] += rr.x * zz.y + rr.y * zz.x;
+            part[5 * k + 2] += v.x * zz.x - v.y * zz.y;
+            part[5 * k + 3] += v.x * zz.y + v.y * zz.x;
+            part[5 * k + 4] += rr.x * rr.x + rr.y * rr.y;
           } else {
             const double2 bv = b[idx];
             const double2 d = ctl.dinv[row];
@@ -1469,6 +1543,7 @@ const void* nbe_fn(int mode) {
     case kResid: return nbe_kernel<K, kResid>();
     case kResidNR: return nbe_kernel<K, kResidNR>();
     case kSmooth: return nbe_kernel<K, kSmooth>();
+    case kCgDot: return nbe_kernel<K, kCgDot>();
     default: return nbe_kernel<K, kSmoothDot>();
   }
 }
@@ -3311,9 +3386,84 @@ ect_part* create_part_assembled(ect_mesh* m, const ect_materials& mats, const in
 
 namespace {
 
+// Chronopoulos-Gear COCG vector kernels (distributed solve): owned rows, a
+// thread owns CW adjacent columns of a row (as k_update).
+// (re)start of the masked columns: [x = 0, r = b when fresh]; z = D^-1 r; p = s = 0
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_cg_init(const double2* __restrict__ b, double2* __restrict__ x, double2* __restrict__ r,
+          double2* __restrict__ z, double2* __restrict__ p, double2* __restrict__ sv,
+          const double2* __restrict__ dinv, unsigned mask, int fresh, KrylovCtl ctl) {
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / KH;
+    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);
+    const double2 d = dinv[i];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) {
+      if (!((mask >> (kb + c)) & 1u)) continue;
+      const int64_t idx = i * K + kb + c;
+      double2 rv;
+      if (fresh) {
+        rv = b[idx];
+        x[idx] = make_double2(0.0, 0.0);
+        r[idx] = rv;
+      } else {
+        rv = r[idx];
+      }
+      z[idx] = cmul(d, rv);
+      p[idx] = sv[idx] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// one fused step (active columns): p = z + beta p, s = w + beta s (s = A p by
+// recurrence), x += alpha p, r -= alpha s, z = D^-1 r
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+k_cg_step(double2* __restrict__ x, double2* __restrict__ r, double2* __restrict__ z,
+          double2* __restrict__ p, double2* __restrict__ sv, const double2* __restrict__ w,
+          const double2* __restrict__ dinv, KrylovCtl ctl) {
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
+  if (*ctl.n_active == 0) return;
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  bool act[CW];
+  double2 alpha[CW], beta[CW];
+#pragma unroll
+  for (int c = 0; c < CW; ++c) {
+    const RhsState& st = ctl.st[kb + c];
+    act[c] = st.status == kActive;
+    alpha[c] = st.alpha;
+    beta[c] = st.beta;
+  }
+  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / KH;
+    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);
+    const double2 d = dinv[i];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) {
+      if (!act[c]) continue;
+      const int64_t idx = i * K + kb + c;
+      const double2 pv = cadd(z[idx], cmul(beta[c], p[idx]));
+      const double2 svv = cadd(w[idx], cmul(beta[c], sv[idx]));
+      p[idx] = pv;
+      sv[idx] = svv;
+      x[idx] = cadd(x[idx], cmul(alpha[c], pv));
+      const double2 rv = csub(r[idx], cmul(alpha[c], svv));
+      r[idx] = rv;
+      z[idx] = cmul(d, rv);
+    }
+  }
+}
+
 template <int K>
 struct PartState {
-  DevBuf<double2> b, x, r, p, q;
+  DevBuf<double2> b, x, r, p, q, z, sv;  // q: w = A z (and the true residual)
   DevBuf<RhsState> st;
   DevBuf<int> n_active;
   DevBuf<unsigned> counter;
@@ -3330,7 +3480,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
   for (int r = 0; r < R; ++r)
     if (parts[r]->ctx != ctx) fail(ECT_ERR_SOLVER, "dist_solve: in-process parts must share a context");
   if (comm && R != 1) fail(ECT_ERR_SOLVER, "dist_solve: with a communicator each process owns one part");
-  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], kCocg), kBlock);
+  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], kCgDot), kBlock);
   const int grid_v = DK::vec_grid(ctx);
   const int grid_max = std::max(grid_s, grid_v);
   const int64_t na_g = parts[0]->na_global;
@@ -3341,10 +3491,12 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
     const HaloPlan& H = parts[r]->plan;
     const int64_t NL = H.n_local();
     PartState<K>& P = S[r];
-    P.b.alloc(NL * K); P.x.alloc(NL * K); P.r.alloc(NL * K); P.p.alloc(NL * K); P.q.alloc(NL * K);
-    for (auto* v : {&P.b, &P.x, &P.r, &P.p, &P.q}) CK(cudaMemsetAsync(v->p, 0, v->bytes(), s));
+    for (auto* v : {&P.b, &P.x, &P.r, &P.p, &P.q, &P.z, &P.sv}) {
+      v->alloc(NL * K);
+      CK(cudaMemsetAsync(v->p, 0, v->bytes(), s));
+    }
     P.st.alloc(K); P.n_active.alloc(1); P.counter.alloc(1);
-    P.partial.alloc((size_t)grid_max * 4 * K); P.red.alloc(4 * K);
+    P.partial.alloc((size_t)grid_max * 5 * K); P.red.alloc(5 * K);
     CK(cudaMemsetAsync(P.st.p, 0, P.st.bytes(), s));
     CK(cudaMemsetAsync(P.counter.p, 0, sizeof(unsigned), s));
     CK(cudaMemsetAsync(P.n_active.p, 0, sizeof(int), s));
@@ -3428,7 +3580,7 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
     v.n_nodes = hi;
     const double2* xp = (S[r].*xin).p;
     double2* yp = (S[r].*yout).p;
-    const double2* bp = with_b ? S[r].b.p : nullptr;
+    const double2* bp = !with_b ? nullptr : mode == kCgDot ? S[r].r.p : S[r].b.p;
     KrylovCtl c = S[r].ctl;
     c.red_add = add ? 1 : 0;
     void* args[] = {&v, &xp, &yp, &bp, &c};
@@ -3448,20 +3600,21 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
     CK(cudaEventCreateWithFlags(&ctx->ev_h1, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_h2, cudaEventDisableTiming));
   }
+  // w = A z with the fused dots (b slot = r), halo of z overlapped
   auto spmv_overlapped = [&](DevBuf<double2> PartState<K>::*xin,
                              DevBuf<double2> PartState<K>::*yout) {
     halo(xin, overlap ? ctx->halo_stream : s);
     for (int r = 0; r < R; ++r) {
       const ect_part* P = parts[r];
-      if (P->int_hi > P->int_lo) spmv_rows(kCocg, xin, yout, false, P->int_lo, P->int_hi, false, r);
+      if (P->int_hi > P->int_lo) spmv_rows(kCgDot, xin, yout, true, P->int_lo, P->int_hi, false, r);
     }
     if (overlap) CK(cudaStreamWaitEvent(s, ctx->ev_h2, 0));
     for (int r = 0; r < R; ++r) {
       const ect_part* P = parts[r];
       const bool any = P->int_hi > P->int_lo;
-      if (P->int_lo > 0) spmv_rows(kCocg, xin, yout, false, 0, P->int_lo, any, r);
+      if (P->int_lo > 0) spmv_rows(kCgDot, xin, yout, true, 0, P->int_lo, any, r);
       if (P->int_hi < P->plan.L)
-        spmv_rows(kCocg, xin, yout, false, any ? P->int_hi : P->int_lo, P->plan.L,
+        spmv_rows(kCgDot, xin, yout, true, any ? P->int_hi : P->int_lo, P->plan.L,
                   any || P->int_lo > 0, r);
     }
   };
@@ -3471,18 +3624,23 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
       if (what == kFinAlpha) k_fin<K, kFinAlpha><<<1, 32, 0, s>>>(c, mask, fresh);
       else if (what == kFinUpdate) k_fin<K, kFinUpdate><<<1, 32, 0, s>>>(c, mask, fresh);
       else if (what == kFinStart) k_fin<K, kFinStart><<<1, 32, 0, s>>>(c, mask, fresh);
+      else if (what == kFinCg) k_fin<K, kFinCg><<<1, 32, 0, s>>>(c, mask, fresh);
+      else if (what == kFinCgStart) k_fin<K, kFinCgStart><<<1, 32, 0, s>>>(c, mask, fresh);
       else k_fin<K, kFinResid><<<1, 32, 0, s>>>(c, mask, fresh);
       CK_LAUNCH();
     }
   };
+  // Chronopoulos-Gear COCG: one reduction (r^T z, w^T z, ||r||) per iteration
   auto start = [&](unsigned mask, int fresh) {
     for (int r = 0; r < R; ++r) {
-      const HaloPlan& H = parts[r]->plan;
-      DK::start(ctx, grid_v, H.n_local(), S[r].b.p, S[r].x.p, S[r].r.p, S[r].p.p, parts[r]->dinv.p,
-                mask, fresh, S[r].ctl);
+      k_cg_init<K><<<grid_v, kBlock, 0, s>>>(S[r].b.p, S[r].x.p, S[r].r.p, S[r].z.p, S[r].p.p,
+                                             S[r].sv.p, parts[r]->dinv.p, mask, fresh, S[r].ctl);
+      CK_LAUNCH();
     }
-    allreduce(4 * K);
-    fin(kFinStart, mask, fresh);
+    for (int r = 0; r < R; ++r) CK(cudaMemsetAsync(S[r].n_active.p, 0xff, sizeof(int), s));
+    spmv_overlapped(&PartState<K>::z, &PartState<K>::q);
+    allreduce(5 * K);
+    fin(kFinCgStart, mask, fresh);
   };
 
   const unsigned all = (K == 32) ? 0xffffffffu : ((1u << K) - 1u);
@@ -3493,26 +3651,32 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
   std::vector<RhsState> hs(K);
   int* flag = ctx->pinned_flag;
   const int chunk = 16;
+  cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
   for (int round = 0;; ++round) {
-    for (int launched = 0; opt.max_iter > 0 && launched <= opt.max_iter + chunk;) {
+    int polls = 0;
+    for (int launched = 0; opt.max_iter > 0 && launched <= opt.max_iter + 2 * chunk;) {
       for (int it = 0; it < chunk; ++it) {
-        spmv_overlapped(&PartState<K>::p, &PartState<K>::q);
-        allreduce(2 * K);
-        fin(kFinAlpha, 0, 0);
-        for (int r = 0; r < R; ++r)
-          DK::update(ctx, grid_v, parts[r]->plan.n_local(), S[r].r.p, S[r].q.p,
-                     parts[r]->dinv.p, S[r].ctl);
-        allreduce(3 * K);
-        fin(kFinUpdate, 0, 0);
-        for (int r = 0; r < R; ++r)
-          DK::pupdate(ctx, grid_v, parts[r]->plan.n_local(), S[r].x.p, S[r].r.p, S[r].p.p,
-                      parts[r]->dinv.p, S[r].ctl);
+        for (int r = 0; r < R; ++r) {
+          k_cg_step<K><<<grid_v, kBlock, 0, s>>>(S[r].x.p, S[r].r.p, S[r].z.p, S[r].p.p,
+                                                 S[r].sv.p, S[r].q.p, parts[r]->dinv.p, S[r].ctl);
+          CK_LAUNCH();
+        }
+        spmv_overlapped(&PartState<K>::z, &PartState<K>::q);  // w = A z, fused dots
+        allreduce(5 * K);                                       // the one reduction
+        fin(kFinCg, 0, 0);
       }
       launched += chunk;
-      CK(cudaMemcpyAsync(flag, S[0].n_active.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      if (*flag == 0) break;
+      // poll the active count one chunk behind (the next chunk is queued first)
+      CK(cudaMemcpyAsync(flag + (polls & 1), S[0].n_active.p, sizeof(int),
+                         cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(poll_ev[polls & 1], s));
+      ++polls;
+      if (polls >= 2) {
+        CK(cudaEventSynchronize(poll_ev[(polls - 2) & 1]));
+        if (flag[(polls - 2) & 1] == 0) break;
+      }
     }
+    CK(cudaStreamSynchronize(s));
     // true residual (iterative.cpp:208-216): q <- b - A x, norms across parts
     CK(cudaMemcpyAsync(hs.data(), S[0].st.p, K * sizeof(RhsState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));  // statuses are identical on every part

@@ -25,7 +25,7 @@ m = w.mesh()
 ctx = ect.Context(0)
 mesh = ect.Mesh(ctx, m.xyz, m.tets, m.region)
 p, r, two = mesh.materials(w.physics)
-zs = [w.positions[i] for i in (20, 26, 31, 36)][: max(1, k // 2)]
+zs = [w.positions[i] for i in (20, 26, 31, 36, 10, 44, 5, 58)][: max(1, k // 2)]
 zz = [z for z in zs for _ in (1, 2)][:k]
 which = [c for _ in zs for c in (1, 2)][:k]
 b = torch.from_numpy(mesh.rhs(w.coil, zz, which, w.amplitude)).cuda()

@@ -31,7 +31,9 @@ def test_partitioned_solve_matches_single(ctx, splits):
     comp = conductor_components(g["tets"], g["region"], g["cond_forward"])
     for c in range(2):
         assert rd[c]["converged"] and rd[c]["residual"] <= 1e-10
-        assert abs(rd[c]["iterations"] - r1[c]["iterations"]) <= 3
+        # the partitioned solve is the single-reduction (Chronopoulos-Gear)
+        # form of the same Jacobi-COCG: equal in exact arithmetic
+        assert abs(rd[c]["iterations"] - r1[c]["iterations"]) <= max(3, 0.03 * r1[c]["iterations"])
         ea, ev = solution_errors(xd[:, c], x1[:, c], m.n_nodes, comp)
         assert ea <= 1e-8 and ev <= 1e-8, (ea, ev)
         ea, ev = solution_errors(xd[:, c], g["primary_x"][c], m.n_nodes, comp)
