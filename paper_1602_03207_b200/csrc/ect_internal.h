@@ -75,6 +75,8 @@ struct RhsState {
   int status;     // kActive / kConverged / kBreakdown / kMaxIter / kZeroRhs
   int xpend;      // COCG: x += alpha p still owed (applied by the next p-update)
   int pad_;
+  double rbest;   // BiCGStab: smallest recurrence residual since the last (re)start
+  double pad2_;
 };
 enum RhsStatus : int { kActive = 0, kConverged = 1, kBreakdown = 2, kMaxIter = 3, kZeroRhs = 4 };
 

@@ -869,11 +869,22 @@ __global__ void k_sell_fill(int64_t n_slots, const int* __restrict__ perm,
 // block j of the chunk's nodes stored contiguously (1 KB per plane), padded to
 // the chunk's largest degree with zero blocks. A warp's block loads are
 // contiguous runs instead of 16-32 scattered 64-byte pieces.
-template <int G, int K, int MODE, int MINB, int CL, int PFD = 0>
-__global__ void __launch_bounds__(kBlock, MINB)
+//
+// FLAT (wide batches, G == CL: one block lane per node): the NPW nodes of a
+// warp lie in one 32-node chunk, so the block loop runs the chunk's width for
+// every lane, unpredicated (padding slots are zero blocks); only the column
+// index is fetched one step ahead, and a step issues its three block planes
+// and its x gathers together. Without the register copy of a pipelined block
+// the kernel keeps ~108 registers and its loads per step stay at the L1
+// writeback floor (every 256-bit load writes 1 KB per warp into registers:
+// 128 B per clock per SM bounds this kernel, not DRAM; ncu r02).
+template <int G, int K, int MODE, int MINB, int CL, int PFD = 0, int BLOCK = kBlock,
+          bool FLAT = false>
+__global__ void __launch_bounds__(BLOCK, MINB)
 k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           const double2* __restrict__ b, KrylovCtl ctl) {
   static_assert(G % CL == 0 && K % CL == 0, "lane split");
+  static_assert(!FLAT || G == CL, "the flat loop has one block lane per node");
   constexpr int GB = G / CL;   // block lanes per node
   constexpr int KL = K / CL;   // right-hand sides per lane
   constexpr int NVL0 = mode_nv(MODE, KL), NVL = NVL0 > 0 ? NVL0 : 1;  // per lane
@@ -905,6 +916,57 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_double2(0.0, 0.0);
     }
     int cf_i = -1;
+    if constexpr (FLAT) {
+      const int c32 = (int)(wn >> 5);
+      const int o32 = A.e_off[c32];
+      const int w32 = (A.e_off[c32 + 1] - o32) >> 5;
+      const int sbase = o32 + (int)(i & 31);
+      constexpr int LINES = NPW >= 4 ? NPW / 4 : 1;  // 128-B lines per plane row of the warp
+      const char* pf = nullptr;
+      int pf_stride = 0;
+      if constexpr (PFD > 0) {
+        if (lane < 3 * LINES) {
+          pf = reinterpret_cast<const char*>(A.blk + 4 * ((int64_t)(lane / LINES) * A.nblk + o32 +
+                                                          (int)(wn & 31)) +
+                                             16 * (lane % LINES));
+          pf_stride = 32 * 32;
+        } else if (lane == 3 * LINES) {
+          pf = reinterpret_cast<const char*>(A.blk_col + o32 + (int)(wn & 31));
+          pf_stride = 32 * 4;
+        }
+      }
+      int m = ldg_i(A.blk_col + sbase);
+      for (int j = 0; j < w32; ++j) {
+        if constexpr (PFD > 0) {
+          if (pf && j + PFD < w32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)(j + PFD) * pf_stride));
+        }
+        const int q = sbase + 32 * j;
+        double B[3][3], Im[3];
+        load_block(A, q, B, Im);
+        const double2* xm = x + (int64_t)3 * m * K + kc;
+        double2 xp[3][KL];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int k = 0; k < KL; k += 2) ld4x(xm + d * K + k, xp[d][k], xp[d][k + 1]);
+        if (j + 1 < w32) m = ldg_i(A.blk_col + q + 32);
+#pragma unroll
+        for (int k = 0; k < KL; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double2 s = acc[c][k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              s.x += B[c][d] * xp[d][k].x;
+              s.y += B[c][d] * xp[d][k].y;
+            }
+            s.x -= Im[c] * xp[c][k].y;
+            s.y += Im[c] * xp[c][k].x;
+            acc[c][k] = s;
+          }
+      }
+    }
     if (valid) {
       // sliced-ELL blocks: block j of node i at slot off[c] + 32 j + (i mod 32)
       const int c32 = (int)(i >> 5);
@@ -916,7 +978,7 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
       int q = sbase + 32 * bl;
       int m_nx = 0;
       double B_nx[3][3], Im_nx[3];
-      if (q < be) {
+      if (!FLAT && q < be) {
         m_nx = ldg_i(A.blk_col + q);
         load_block(A, q, B_nx, Im_nx);
       }
@@ -940,7 +1002,7 @@ k_nbe_spmv(NbView A, const double2* __restrict__ x, double2* __restrict__ y,
           pf_stride = 32 * 4;
         }
       }
-      for (; q < be; q += GS) {
+      for (; !FLAT && q < be; q += GS) {
         if constexpr (PFD > 0) {
           const int row0 = ((q - sbase) >> 5) - bl + PFD * GB;
           if (pf) {
@@ -1528,15 +1590,20 @@ NbView nb_view(const ect_matrix* a) {
 
 // Default NB-E launch configuration per batch width (measured on configs[1],
 // B200): G lanes per node, CTAs per SM, CL column lanes, L2 prefetch distance.
+struct KFn {
+  const void* fn;
+  int block;  // threads per CTA the kernel is compiled for
+};
 template <int K, int MODE>
-const void* nbe_kernel() {
-  if constexpr (K <= 2) return (const void*)k_nbe_spmv<2, K, MODE, 2, 1, 2>;
-  else if constexpr (K == 4) return (const void*)k_nbe_spmv<2, K, MODE, 2, 2, 4>;
-  else if constexpr (K == 8) return (const void*)k_nbe_spmv<4, K, MODE, 2, 4, 4>;
-  else return (const void*)k_nbe_spmv<8, K, MODE, 2, 8>;
+KFn nbe_kernel() {
+  if constexpr (K <= 2) return {(const void*)k_nbe_spmv<2, K, MODE, 2, 1, 2>, kBlock};
+  else if constexpr (K == 4) return {(const void*)k_nbe_spmv<2, K, MODE, 2, 2, 4>, kBlock};
+  else if constexpr (K == 8)  // flat loop, 2 columns per lane (lab: 0.282 vs 0.327 ms)
+    return {(const void*)k_nbe_spmv<4, K, MODE, 2, 4, 2, kBlock, true>, kBlock};
+  else return {(const void*)k_nbe_spmv<8, K, MODE, 2, 8>, kBlock};
 }
 template <int K>
-const void* nbe_fn(int mode) {
+KFn nbe_fn(int mode) {
   switch (mode) {
     case kPlain: return nbe_kernel<K, kPlain>();
     case kCocg: return nbe_kernel<K, kCocg>();
@@ -1566,6 +1633,21 @@ const void* csr_fn(int mode) {
 // lanes per row of the CSR kernel (grid sizing)
 template <int K>
 constexpr int csr_lanes() { return K == 1 ? 16 : (K / 2) * (K >= 16 ? 1 : 16 / K); }
+// Coarse multigrid levels: Galerkin rows are long (60-200 entries) and the
+// levels are small, so a whole warp streams one row (32 lanes = K/2 column
+// pairs x 64/K entry lanes): the serial chain of dependent column -> gather
+// loads per lane is what those launches cost (35 us for a 5k-row level with
+// 2 entry lanes, r02 launch list).
+template <int K>
+const void* csr_row_fn(int mode) {
+  if constexpr (K == 1) {
+    return mode == kResidNR ? (const void*)k_spmv<32, 1, kResidNR> : (const void*)k_spmv<32, 1, kSmooth>;
+  } else {
+    constexpr int E = K >= 64 ? 1 : 64 / K;
+    return mode == kResidNR ? (const void*)k_spmv_v<K, E, kResidNR>
+                            : (const void*)k_spmv_v<K, E, kSmooth>;
+  }
+}
 template <int K>
 const void* sell_fn(int mode) {
   return mode == kPlain  ? (const void*)k_sell_spmv<K, kPlain>
@@ -1595,7 +1677,8 @@ struct Dispatch {
         v.nblk = a->nbe_slots;
         v.e_off = a->nbe_off.p;
         void* args[] = {&v, &x, &y, &b, &ctl};
-        CK(cudaLaunchKernel(nbe_fn<K>(mode), dim3(grid), dim3(kBlock), args, 0, s));
+        const KFn f = nbe_fn<K>(mode);
+        CK(cudaLaunchKernel(f.fn, dim3(grid), dim3(f.block), args, 0, s));
         return;
       }
       case Store::kSell: {
@@ -1617,10 +1700,11 @@ struct Dispatch {
   // plain complex CSR (also the coarse multigrid levels)
   static void csr(ect_ctx* ctx, int mode, int grid, int64_t n, const int* rp, const int* cl,
                   const double2* vl, const double2* x, double2* y, const double2* b,
-                  KrylovCtl ctl) {
+                  KrylovCtl ctl, bool warp_per_row = false) {
     void* args[] = {(void*)&n, (void*)&rp, (void*)&cl, (void*)&vl, (void*)&x, (void*)&y,
                     (void*)&b, (void*)&ctl};
-    CK(cudaLaunchKernel(csr_fn<K>(mode), dim3(grid), dim3(kBlock), args, 0, ctx->stream));
+    const void* fn = warp_per_row ? csr_row_fn<K>(mode) : csr_fn<K>(mode);
+    CK(cudaLaunchKernel(fn, dim3(grid), dim3(kBlock), args, 0, ctx->stream));
   }
   static void update(ect_ctx* ctx, int grid, int64_t n, double2* r, const double2* q,
                      const double2* dinv, KrylovCtl ctl) {
@@ -1639,7 +1723,7 @@ struct Dispatch {
   }
   static int spmv_grid(ect_ctx* ctx, int mode, const ect_matrix* a) {
     switch (store_of(a, mode)) {
-      case Store::kNbe: return grid_for(ctx, nbe_fn<K>(mode), kBlock);
+      case Store::kNbe: return grid_for(ctx, nbe_fn<K>(mode).fn, nbe_fn<K>(mode).block);
       case Store::kSell: return grid_for(ctx, sell_fn<K>(mode), kBlock);
       default: return grid_for(ctx, csr_fn<K>(mode), kBlock);
     }
@@ -2028,6 +2112,8 @@ k_bi_dot(int64_t n, const double2* __restrict__ a, const double2* __restrict__ b
   }
 }
 
+constexpr double kBiGrowth = 1e4;  // recurrence residual / best since restart -> restart
+
 // x += alpha p_hat + omega s_hat ; r = s - omega t ; rho_new = (r_hat, r), ||r||
 template <int K>
 __global__ void __launch_bounds__(kBlock)
@@ -2069,11 +2155,16 @@ k_bi_x(int64_t n, double2* __restrict__ x, double2* __restrict__ r,
       const double2 rho_new = make_double2(tot[NVL * c], tot[NVL * c + 1]);
       s.rnorm = sqrt(tot[NVL * c + 2]);
       s.iters += 1;
+      if (s.rnorm < s.rbest) s.rbest = s.rnorm;
       if (s.rnorm <= ctl.tol * s.bnorm) {
         s.status = kConverged;
       } else if (s.iters >= ctl.max_iter) {
         s.status = kMaxIter;
-      } else if ((rho_new.x == 0.0 && rho_new.y == 0.0) || (s.omega.x == 0.0 && s.omega.y == 0.0)) {
+      } else if ((rho_new.x == 0.0 && rho_new.y == 0.0) || (s.omega.x == 0.0 && s.omega.y == 0.0) ||
+                 !(s.rnorm <= kBiGrowth * s.rbest)) {
+        // Lanczos (near-)breakdown, or the recurrence residual has grown far
+        // above its best value (also NaN): restart from the true residual
+        // before the drift reaches x
         s.status = kBreakdown;
       } else {
         s.beta = cmul(cdiv(rho_new, s.rho), cdiv(s.alpha, s.omega));
@@ -2132,7 +2223,7 @@ k_bi_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x,
           s.bnorm = sqrt(rr);
           s.iters = 0;
         }
-        s.rnorm = sqrt(rr);
+        s.rnorm = s.rbest = sqrt(rr);
         s.rho = make_double2(rr, 0.0);
         s.alpha = s.omega = make_double2(1.0, 0.0);
         s.beta = make_double2(0.0, 0.0);
@@ -2323,11 +2414,16 @@ __device__ __forceinline__ void load_block32(const Nb32& A, int64_t q, float (&B
 // KL = K / CL columns per lane, even or 1). Modes:
 //  kResidNR  : y32 = b - A x                  (b fp64, x fp32, y fp32)
 //  kSmoothDot: z = x + omega D^-1 (b - A x), rho partials b^T z (z fp64)
-template <int G, int K, int MODE, int MINB, int CL>
-__global__ void __launch_bounds__(kBlock, MINB)
+// FLAT (wide batches, one block lane per node): the unpredicated chunk-width
+// loop of k_nbe_spmv; at ~63 registers the SM holds 32 warps, which is what
+// hides the gather latency here (lab: 0.147 vs 0.347 ms at k = 8).
+template <int G, int K, int MODE, int MINB, int CL, int BLOCK = kBlock, bool FLAT = false,
+          int PFD = 0>
+__global__ void __launch_bounds__(BLOCK, MINB)
 k_nbe32(Nb32 A, const float2* __restrict__ x, void* __restrict__ yv,
         const double2* __restrict__ b, KrylovCtl ctl) {
   static_assert(G % CL == 0 && K % CL == 0, "lane split");
+  static_assert(!FLAT || G == CL, "the flat loop has one block lane per node");
   static_assert(MODE == kResidNR || MODE == kSmoothDot, "fp32 smoothing modes");
   constexpr int GB = G / CL, KL = K / CL;
   constexpr int NVL = MODE == kSmoothDot ? 2 * KL : 1, NV = NVL * CL;
@@ -2350,6 +2446,57 @@ k_nbe32(Nb32 A, const float2* __restrict__ x, void* __restrict__ yv,
 #pragma unroll
     for (int k = 0; k < KL; ++k) acc[0][k] = acc[1][k] = acc[2][k] = accv[k] = make_float2(0.f, 0.f);
     int cf_i = -1;
+    if constexpr (FLAT) {
+      const int c32 = (int)(wn >> 5);
+      const int o32 = A.e_off[c32];
+      const int w32 = (A.e_off[c32 + 1] - o32) >> 5;
+      const int sbase = o32 + (int)(i & 31);
+      constexpr int LINES = NPW >= 8 ? NPW / 8 : 1;  // 128-B lines per fp32 plane row of the warp
+      const char* pf = nullptr;
+      int pf_stride = 0;
+      if constexpr (PFD > 0) {
+        if (lane < 3 * LINES) {
+          pf = reinterpret_cast<const char*>(A.blk + 4 * ((int64_t)(lane / LINES) * A.nslots + o32 +
+                                                          (int)(wn & 31)) +
+                                             32 * (lane % LINES));
+          pf_stride = 32 * 16;
+        } else if (lane == 3 * LINES) {
+          pf = reinterpret_cast<const char*>(A.blk_col + o32 + (int)(wn & 31));
+          pf_stride = 32 * 4;
+        }
+      }
+      int m = ldg_i(A.blk_col + sbase);
+      for (int j = 0; j < w32; ++j) {
+        if constexpr (PFD > 0) {
+          if (pf && j + PFD < w32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)(j + PFD) * pf_stride));
+        }
+        const int q = sbase + 32 * j;
+        float B[3][3], Im[3];
+        load_block32(A, q, B, Im);
+        const float2* xm = x + (int64_t)3 * m * K + kc;
+        float2 xp[3][KL];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int k = 0; k < KL; k += 2) ld2xf(xm + d * K + k, xp[d][k], xp[d][k + 1]);
+        if (j + 1 < w32) m = ldg_i(A.blk_col + q + 32);
+#pragma unroll
+        for (int k = 0; k < KL; ++k)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float2 s = acc[c][k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              s.x = fmaf(B[c][d], xp[d][k].x, s.x);
+              s.y = fmaf(B[c][d], xp[d][k].y, s.y);
+            }
+            s.x = fmaf(-Im[c], xp[c][k].y, s.x);
+            s.y = fmaf(Im[c], xp[c][k].x, s.y);
+            acc[c][k] = s;
+          }
+      }
+    }
     if (valid) {
       const int c32 = (int)(i >> 5);
       const int o32 = A.e_off[c32];
@@ -2359,11 +2506,11 @@ k_nbe32(Nb32 A, const float2* __restrict__ x, void* __restrict__ yv,
       int q = sbase + 32 * bl;
       int m_nx = 0;
       float B_nx[3][3], Im_nx[3];
-      if (q < be) {
+      if (!FLAT && q < be) {
         m_nx = ldg_i(A.blk_col + q);
         load_block32(A, q, B_nx, Im_nx);
       }
-      for (; q < be; q += GS) {
+      for (; !FLAT && q < be; q += GS) {
         const int m = m_nx;
         float B[3][3], Im[3];
 #pragma unroll
@@ -2492,11 +2639,13 @@ k_nbe32(Nb32 A, const float2* __restrict__ x, void* __restrict__ yv,
 }
 
 template <int K, int MODE>
-const void* nbe32_fn() {
-  if constexpr (K <= 2) return (const void*)k_nbe32<2, K, MODE, 3, 1>;
-  else if constexpr (K == 4) return (const void*)k_nbe32<4, K, MODE, 3, 2>;
-  else if constexpr (K == 8) return (const void*)k_nbe32<8, K, MODE, 2, 4>;
-  else return (const void*)k_nbe32<8, K, MODE, 2, 8>;
+KFn nbe32_fn() {
+  if constexpr (K <= 2) return {(const void*)k_nbe32<2, K, MODE, 3, 1>, kBlock};
+  else if constexpr (K == 4) return {(const void*)k_nbe32<4, K, MODE, 3, 2>, kBlock};
+  else if constexpr (K == 8) {  // 64 registers (32 warps/SM); the dot epilogue needs 73
+    constexpr int MINB = MODE == kSmoothDot ? 7 : 8;
+    return {(const void*)k_nbe32<4, K, MODE, MINB, 4, 128, true, 2>, 128};
+  } else return {(const void*)k_nbe32<8, K, MODE, 2, 8>, kBlock};
 }
 
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ out) {
@@ -2678,17 +2827,17 @@ struct Cycle {
         CK_LAUNCH();
         note_launch(ctx, 2);
       }
-      grid32[kResidNR] = grid_for(ctx, nbe32_fn<K, kResidNR>(), kBlock);
-      grid32[kSmoothDot] = grid_for(ctx, nbe32_fn<K, kSmoothDot>(), kBlock);
+      grid32[kResidNR] = grid_for(ctx, nbe32_fn<K, kResidNR>().fn, nbe32_fn<K, kResidNR>().block);
+      grid32[kSmoothDot] =
+          grid_for(ctx, nbe32_fn<K, kSmoothDot>().fn, nbe32_fn<K, kSmoothDot>().block);
     }
     for (int mode : {kResidNR, kSmooth, kSmoothDot}) grid0[mode] = DK::spmv_grid(ctx, mode, a);
     gl.resize(H.lv.size());
-    constexpr int G = csr_lanes<K>();
     for (size_t l = 1; l < H.lv.size(); ++l)
-      for (int mode : {kResidNR, kSmooth}) {
-        const int64_t need = (H.lv[l].n * G + kBlock - 1) / kBlock;
+      for (int mode : {kResidNR, kSmooth}) {  // one warp per coarse row
+        const int64_t need = (H.lv[l].n * 32 + kBlock - 1) / kBlock;
         gl[l][mode] = (int)std::max<int64_t>(
-            1, std::min<int64_t>(need, grid_for(ctx, csr_fn<K>(mode), kBlock)));
+            1, std::min<int64_t>(need, grid_for(ctx, csr_row_fn<K>(mode), kBlock)));
       }
     // work vectors for this batch width
     if (H.kcap < K) {
@@ -2720,8 +2869,8 @@ struct Cycle {
     c.dinv = a->dinv.p;
     Nb32 v = nb32();
     void* args[] = {&v, (void*)&x, &y, (void*)&b, &c};
-    const void* fn = mode == kResidNR ? nbe32_fn<K, kResidNR>() : nbe32_fn<K, kSmoothDot>();
-    CK(cudaLaunchKernel(fn, dim3(grid32[mode]), dim3(kBlock), args, 0, ctx->stream));
+    const KFn f = mode == kResidNR ? nbe32_fn<K, kResidNR>() : nbe32_fn<K, kSmoothDot>();
+    CK(cudaLaunchKernel(f.fn, dim3(grid32[mode]), dim3(f.block), args, 0, ctx->stream));
   }
   // finest level with fp32 smoothing: b = r (fp64), out = z (fp64), dot always
   void run0_f32(const double2* b, double2* out, KrylovCtl c, bool pre) {
@@ -2758,7 +2907,7 @@ struct Cycle {
     } else {
       AmgLevel& L = H.lv[l];
       c.dinv = L.dinv.p;
-      DK::csr(ctx, mode, gl[l][mode], L.n, L.row_ptr.p, L.col.p, L.val.p, x, y, b, c);
+      DK::csr(ctx, mode, gl[l][mode], L.n, L.row_ptr.p, L.col.p, L.val.p, x, y, b, c, true);
     }
   }
   // out = M_l b; t0 = a free level-0 vector (COCG's q); pre = the level's
@@ -3076,7 +3225,7 @@ NbView part_view(const ect_part* P) {
 }
 
 template <int K>
-const void* part_fn(const ect_part* P, int mode) {
+KFn part_fn(const ect_part* P, int mode) {
   (void)P;
   return nbe_fn<K>(mode);
 }
@@ -3480,7 +3629,8 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
   for (int r = 0; r < R; ++r)
     if (parts[r]->ctx != ctx) fail(ECT_ERR_SOLVER, "dist_solve: in-process parts must share a context");
   if (comm && R != 1) fail(ECT_ERR_SOLVER, "dist_solve: with a communicator each process owns one part");
-  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], kCgDot), kBlock);
+  const int grid_s = grid_for(ctx, part_fn<K>(parts[0], kCgDot).fn,
+                              part_fn<K>(parts[0], kCgDot).block);
   const int grid_v = DK::vec_grid(ctx);
   const int grid_max = std::max(grid_s, grid_v);
   const int64_t na_g = parts[0]->na_global;
@@ -3584,8 +3734,8 @@ void dist_solve_k(ect_part** parts, int R, ect_comm* comm, const double2* b_glob
     KrylovCtl c = S[r].ctl;
     c.red_add = add ? 1 : 0;
     void* args[] = {&v, &xp, &yp, &bp, &c};
-    CK(cudaLaunchKernel(part_fn<K>(parts[r], mode), dim3(grid_s), dim3(kBlock),
-                        args, 0, s));
+    const KFn f = part_fn<K>(parts[r], mode);
+    CK(cudaLaunchKernel(f.fn, dim3(grid_s), dim3(f.block), args, 0, s));
   };
   auto spmv = [&](int mode, DevBuf<double2> PartState<K>::*xin, DevBuf<double2> PartState<K>::*yout,
                   bool with_b) {

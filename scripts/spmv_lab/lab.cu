@@ -249,6 +249,204 @@ k_wide(View A, const double2* __restrict__ x, double2* __restrict__ y) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_shfl: CL = 4 / KL = 2 lanes as k_wide, but the block is loaded ONCE per
+// node (lane cl < 3 loads plane cl) and broadcast with shuffles, so the L1
+// writeback carries each matrix byte once instead of CL times.
+template <int BLOCK, int MINB, int PFD>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_shfl(View A, const double2* __restrict__ x, double2* __restrict__ y) {
+  constexpr int K = 8, KL = 2, CL = 4, NPW = 8;
+  const int lane = threadIdx.x & 31;
+  const int cl = lane % CL, kc = cl * KL;
+  const int lbase = lane & ~3;
+  const int64_t warp = (blockIdx.x * (int64_t)BLOCK + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * BLOCK) >> 5;
+  const int64_t n_groups = (A.n_nodes + NPW - 1) / NPW;
+  for (int64_t gidx = warp; gidx < n_groups; gidx += n_warps) {
+    const int64_t wn = gidx * NPW;
+    const int64_t i = wn + lane / CL;
+    const int c32 = (int)(wn >> 5);
+    const int o32 = A.off[c32];
+    const int w32 = (A.off[c32 + 1] - o32) >> 5;
+    const int sbase = o32 + (int)(i & 31);
+    double2 acc[3][KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) acc[0][k] = acc[1][k] = acc[2][k] = make_double2(0.0, 0.0);
+    constexpr int LINES = 2;
+    const char* pf = nullptr;
+    int pf_stride = 0;
+    if constexpr (PFD > 0) {
+      if (lane < 3 * LINES) {
+        pf = reinterpret_cast<const char*>(A.blk + 4 * ((int64_t)(lane / LINES) * A.nslots + o32 +
+                                                        (int)(wn & 31))) + 128 * (lane % LINES);
+        pf_stride = 32 * 32;
+      } else if (lane == 3 * LINES) {
+        pf = reinterpret_cast<const char*>(A.col + o32 + (int)(wn & 31));
+        pf_stride = 32 * 4;
+      }
+    }
+    // this lane's plane (cl = 3 re-reads plane 2: same address as lane 2, no extra sector)
+    const double* mine = A.blk + 4 * ((int64_t)(cl < 3 ? cl : 2) * A.nslots + sbase);
+    int m_nx = ldg_i(A.col + sbase);
+    double v_nx[4];
+    ld4s(mine, v_nx);
+    for (int j = 0; j < w32; ++j) {
+      if constexpr (PFD > 0) {
+        if (pf && j + PFD < w32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)(j + PFD) * pf_stride));
+      }
+      const int m = m_nx;
+      double v[4] = {v_nx[0], v_nx[1], v_nx[2], v_nx[3]};
+      XV<KL> X;
+      load_x<K, KL>(x, m, kc, X);
+      if (j + 1 < w32) {
+        m_nx = ldg_i(A.col + sbase + 32 * (j + 1));
+        ld4s(mine + 4 * 32 * (int64_t)(j + 1), v_nx);
+      }
+      double p[3][4];
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p[pl][e] = __shfl_sync(0xffffffffu, v[e], lbase | pl);
+      Blk b;
+      b.B[0][0] = p[0][0]; b.B[0][1] = p[0][1]; b.B[0][2] = p[0][2];
+      b.B[1][0] = p[0][3]; b.B[1][1] = p[1][0]; b.B[1][2] = p[1][1];
+      b.B[2][0] = p[1][2]; b.B[2][1] = p[1][3]; b.B[2][2] = p[2][0];
+      b.Im[0] = p[2][1]; b.Im[1] = p[2][2]; b.Im[2] = p[2][3];
+      fma_block<KL>(b, X, acc);
+    }
+    if (i < A.n_nodes) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double2* yr = y + (3 * i + c) * K + kc;
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(yr), "d"(acc[c][0].x),
+                     "d"(acc[c][0].y), "d"(acc[c][1].x), "d"(acc[c][1].y)
+                     : "memory");
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_dsplit<KL>: lanes = (node, RHS group h of KL columns, block column d).
+// Lane d < 3 owns column d of every block of its node: one 256-bit load of the
+// column plane (B[d][d], B[d+1][d], B[d+2][d], Im[d]) (rows rotated so that the
+// diagonal comes first), the KL values of x component d, and partial sums of
+// rows d, d+1, d+2 (mod 3). Nothing is loaded twice; the three column lanes
+// are summed once per node with two shuffles per value. Lane d = 3 idles.
+template <int KL, int BLOCK, int MINB, int PIPE, int PFD>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_dsplit(View A /* blk = column planes */, const double2* __restrict__ x, double2* __restrict__ y) {
+  constexpr int K = 8, H = K / KL, G = 4 * H, NPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int d = lane & 3, h = (lane >> 2) % H, kc = h * KL;
+  const bool act = d < 3;
+  const int dd = act ? d : 2;
+  const int64_t warp = (blockIdx.x * (int64_t)BLOCK + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * BLOCK) >> 5;
+  const int64_t n_groups = (A.n_nodes + NPW - 1) / NPW;
+  for (int64_t gidx = warp; gidx < n_groups; gidx += n_warps) {
+    const int64_t wn = gidx * NPW;
+    const int64_t i = wn + lane / G;
+    const int c32 = (int)(wn >> 5);
+    const int o32 = A.off[c32];
+    const int w32 = (A.off[c32 + 1] - o32) >> 5;
+    const int sbase = o32 + (int)(i & 31);
+    double2 acc[3][KL];  // rows d, d + 1, d + 2 (mod 3)
+#pragma unroll
+    for (int k = 0; k < KL; ++k) acc[0][k] = acc[1][k] = acc[2][k] = make_double2(0.0, 0.0);
+    constexpr int LINES = NPW >= 4 ? NPW / 4 : 1;
+    const char* pf = nullptr;
+    int pf_stride = 0;
+    if constexpr (PFD > 0) {
+      if (lane < 3 * LINES) {
+        pf = reinterpret_cast<const char*>(A.blk + 4 * ((int64_t)(lane / LINES) * A.nslots + o32 +
+                                                        (int)(wn & 31))) + 128 * (lane % LINES);
+        pf_stride = 32 * 32;
+      } else if (lane == 3 * LINES) {
+        pf = reinterpret_cast<const char*>(A.col + o32 + (int)(wn & 31));
+        pf_stride = 32 * 4;
+      }
+    }
+    const double* mine = A.blk + 4 * ((int64_t)dd * A.nslots + sbase);
+    auto step = [&](const double (&v)[4], const double2 (&xv)[KL]) {
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          acc[r][k].x += v[r] * xv[k].x;
+          acc[r][k].y += v[r] * xv[k].y;
+        }
+        acc[0][k].x -= v[3] * xv[k].y;
+        acc[0][k].y += v[3] * xv[k].x;
+      }
+    };
+    auto loadx = [&](int m, double2 (&xv)[KL]) {
+      const double2* xm = x + ((int64_t)3 * m + dd) * K + kc;
+#pragma unroll
+      for (int k = 0; k < KL; k += 2) ld4x(xm + k, xv[k], xv[k + 1]);
+    };
+    if constexpr (PIPE == 0) {
+      int m = ldg_i(A.col + sbase);
+      for (int j = 0; j < w32; ++j) {
+        if constexpr (PFD > 0) {
+          if (pf && j + PFD < w32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)(j + PFD) * pf_stride));
+        }
+        double v[4];
+        double2 xv[KL];
+        if (act) {
+          ld4s(mine + 4 * 32 * (int64_t)j, v);
+          loadx(m, xv);
+        }
+        if (j + 1 < w32) m = ldg_i(A.col + sbase + 32 * (j + 1));
+        if (act) step(v, xv);
+      }
+    } else {
+      int m_nx = ldg_i(A.col + sbase);
+      double v_nx[4] = {0, 0, 0, 0};
+      if (act) ld4s(mine, v_nx);
+      for (int j = 0; j < w32; ++j) {
+        if constexpr (PFD > 0) {
+          if (pf && j + PFD < w32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + (int64_t)(j + PFD) * pf_stride));
+        }
+        const int m = m_nx;
+        const double v[4] = {v_nx[0], v_nx[1], v_nx[2], v_nx[3]};
+        double2 xv[KL];
+        if (act) loadx(m, xv);
+        if (j + 1 < w32) {
+          m_nx = ldg_i(A.col + sbase + 32 * (j + 1));
+          if (act) ld4s(mine + 4 * 32 * (int64_t)(j + 1), v_nx);
+        }
+        if (act) step(v, xv);
+      }
+    }
+    // row d total = own acc[0] + acc[1] of lane (d + 2) % 3 + acc[2] of lane (d + 1) % 3
+    const int lb = lane & ~3;
+    const int src1 = lb | ((d + 2) % 3), src2 = lb | ((d + 1) % 3);
+#pragma unroll
+    for (int k = 0; k < KL; ++k) {
+      const double a1x = __shfl_sync(0xffffffffu, acc[1][k].x, src1);
+      const double a1y = __shfl_sync(0xffffffffu, acc[1][k].y, src1);
+      const double a2x = __shfl_sync(0xffffffffu, acc[2][k].x, src2);
+      const double a2y = __shfl_sync(0xffffffffu, acc[2][k].y, src2);
+      acc[0][k].x += a1x + a2x;
+      acc[0][k].y += a1y + a2y;
+    }
+    if (act && i < A.n_nodes) {
+      double2* yr = y + (3 * i + d) * K + kc;
+#pragma unroll
+      for (int k = 0; k < KL; k += 2)
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(yr + k), "d"(acc[0][k].x),
+                     "d"(acc[0][k].y), "d"(acc[0][k + 1].x), "d"(acc[0][k + 1].y)
+                     : "memory");
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the library's current k = 8 kernel (G = 4, CL = 4, KL = 2, one block ahead,
 // predicated loop), kPlain mode — the calibration point (0.435 ms on configs[1])
@@ -530,6 +728,7 @@ struct Variant {
   const void* fn;
   int block;
   bool f32;
+  bool colplanes = false;
 };
 
 template <typename T>
@@ -596,6 +795,17 @@ int main(int argc, char** argv) {
       }
     }
   }
+  // column planes for k_dsplit: plane d = (B[d][d], B[d+1][d], B[d+2][d], Im[d]), rows mod 3
+  std::vector<double> blkc(blk.size());
+  for (int64_t sl = 0; sl < nslots; ++sl) {
+    double f[12];
+    for (int pl = 0; pl < 3; ++pl)
+      for (int e = 0; e < 4; ++e) f[4 * pl + e] = blk[4 * (pl * nslots + sl) + e];
+    for (int d = 0; d < 3; ++d) {
+      for (int r = 0; r < 3; ++r) blkc[4 * (d * nslots + sl) + r] = f[3 * ((d + r) % 3) + d];
+      blkc[4 * (d * nslots + sl) + 3] = f[9 + d];
+    }
+  }
   std::vector<float> blk32(blk.size());
   for (size_t q = 0; q < blk.size(); ++q) blk32[q] = (float)blk[q];
   std::vector<double2> x(3 * n * K);
@@ -607,6 +817,7 @@ int main(int argc, char** argv) {
   int* d_off = dev(off);
   int* d_col = dev(col);
   double* d_blk = dev(blk);
+  double* d_blkc = dev(blkc);
   float* d_blk32 = dev(blk32);
   double2* d_x = dev(x);
   float2* d_x32 = dev(x32);
@@ -618,6 +829,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&d_ref32, x.size() * sizeof(float2)));
   View A{d_off, d_col, d_blk, nslots, n};
   View32 A32{d_off, d_col, d_blk32, nslots, n};
+  View AC{d_off, d_col, d_blkc, nslots, n};
   const double fmt64 = 100.0 * nslots + 4.0 * (n_chunks + 1) + 2.0 * 16.0 * 3 * n * K;
   const double fmt32 = 52.0 * nslots + 4.0 * (n_chunks + 1) + 2.0 * 8.0 * 3 * n * K;
   std::printf("nodes %lld blocks %lld slots %lld (padding %.1f%%)  fp64 format bytes %.3f GB, fp32 %.3f GB\n",
@@ -649,6 +861,33 @@ int main(int argc, char** argv) {
   ADD(8, 128, 2, 0, 4);
   ADD(8, 128, 2, 1, 4);
   ADD(8, 128, 1, 2, 4);
+#define ADDS(BLOCK, MINB, PFD) \
+  vs.push_back({"shfl blk=" #BLOCK " minb=" #MINB " pfd=" #PFD, (const void*)k_shfl<BLOCK, MINB, PFD>, BLOCK, false})
+#define ADDD(KL, BLOCK, MINB, PIPE, PFD)                                                    \
+  vs.push_back({"dsplit KL=" #KL " blk=" #BLOCK " minb=" #MINB " pipe=" #PIPE " pfd=" #PFD, \
+                (const void*)k_dsplit<KL, BLOCK, MINB, PIPE, PFD>, BLOCK, false, true})
+  ADD(2, 256, 3, 0, 4);
+  ADD(2, 128, 6, 0, 4);
+  ADD(2, 128, 7, 0, 4);
+  ADD(2, 256, 2, 0, 2);
+  ADD(2, 256, 2, 0, 6);
+  ADD(2, 256, 2, 0, 8);
+  ADDS(256, 2, 4);
+  ADDS(128, 5, 4);
+  ADDS(128, 6, 4);
+  ADDS(128, 8, 4);
+  ADDD(8, 128, 3, 0, 4);
+  ADDD(8, 128, 3, 1, 4);
+  ADDD(8, 128, 4, 0, 4);
+  ADDD(8, 256, 2, 1, 4);
+  ADDD(4, 128, 4, 0, 4);
+  ADDD(4, 128, 5, 0, 4);
+  ADDD(4, 128, 5, 1, 4);
+  ADDD(4, 128, 6, 0, 4);
+  ADDD(4, 128, 6, 1, 4);
+  ADDD(4, 256, 3, 1, 4);
+  ADDD(2, 128, 8, 0, 4);
+  ADDD(2, 128, 8, 1, 4);
   vs.push_back({"cur32 (library)", (const void*)k_cur32, 256, true});
   ADD32(2, 256, 2, 1, 4);
   ADD32(2, 256, 3, 1, 4);
@@ -663,6 +902,12 @@ int main(int argc, char** argv) {
   ADD32(8, 128, 3, 0, 4);
   ADD32(8, 128, 3, 1, 4);
   ADD32(8, 128, 2, 2, 4);
+  ADD32(2, 256, 4, 0, 4);
+  ADD32(2, 128, 8, 0, 2);
+  ADD32(2, 128, 8, 0, 8);
+  ADD32(2, 128, 8, 0, 0);
+  ADD32(2, 64, 16, 0, 4);
+  ADD32(4, 128, 8, 0, 4);
 
   int dev_id = 0, sms = 0;
   CK(cudaGetDevice(&dev_id));
@@ -683,7 +928,7 @@ int main(int argc, char** argv) {
     const int grid = per_sm * sms;
     void* y = v.f32 ? (void*)d_y32 : (void*)d_y;
     void* xx = v.f32 ? (void*)d_x32 : (void*)d_x;
-    void* args64[] = {&A, &xx, &y};
+    void* args64[] = {v.colplanes ? (void*)&AC : (void*)&A, &xx, &y};
     void* args32[] = {&A32, &xx, &y};
     void** args = v.f32 ? args32 : args64;
     CK(cudaMemset(y, 0xff, x.size() * (v.f32 ? sizeof(float2) : sizeof(double2))));
