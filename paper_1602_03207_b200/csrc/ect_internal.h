@@ -281,6 +281,10 @@ void compute_jacobi(ect_matrix* a);                            // krylov.cu
 void build_nb(ect_mesh* m, ect_matrix* a);                     // krylov.cu (NB format)
 void build_sell(ect_matrix* a, int sigma);                     // krylov.cu (SELL-C-sigma)
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k);  // spmv.cu
+// dst[c * n + i] = src[i * k + cols[c]] for c < n_cols <= 4 (columns of an
+// interleaved [n][k] batch as contiguous vectors, on the context stream)
+void gather_columns(ect_ctx* ctx, const double2* src, int k, const int* cols, int n_cols,
+                    int64_t n, double2* dst);
 void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* which, int n_rhs,
                double amplitude, double2* rhs);                // rhs.cu
 void build_rhs_support(ect_mesh* m, const int* support, int64_t n_support, int region_tag,

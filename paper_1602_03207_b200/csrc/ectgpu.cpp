@@ -922,7 +922,7 @@ struct ect_session {
   ect_matrix* a_primary = nullptr;
   ect_matrix* a_reference = nullptr;
   // right-hand sides and solutions of one batch, kept across calls
-  ect::DevBuf<double2> rhs, xp, xr;
+  ect::DevBuf<double2> rhs, xp, xr, sol;
   ~ect_session() {
     delete a_primary;
     delete a_reference;
@@ -1056,15 +1056,20 @@ int ect_session_solve_positions(ect_session* s, const double* z, int32_t n_pos,
         if (solutions && p0 + np == n_pos) {
           // 4 solution vectors of the last position: primary c1, c2, reference c1, c2
           const int q = np - 1;
+          // columns gathered into contiguous vectors on the device, then ONE
+          // contiguous copy (a strided 16-byte-row copy to the host costs ~10 ms
+          // per vector over PCIe)
           double2* dst = reinterpret_cast<double2*>(solutions);
           const bool dev = ect::is_device_ptr(solutions);
-          const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-          for (int v = 0; v < 4; ++v) {
-            const double2* src = (v < 2 ? xp.p : xr.p) + 2 * q + (v & 1);
-            if (v >= 2 && !s->two_configs) src = xp.p + 2 * q + (v & 1);
-            CK(cudaMemcpy2DAsync(dst + v * N, sizeof(double2), src, k * sizeof(double2),
-                                 sizeof(double2), N, kind, ctx->stream));
+          double2* stage = dst;
+          if (!dev) {
+            s->sol.ensure((size_t)4 * N);
+            stage = s->sol.p;
           }
+          const int cols[2] = {2 * q, 2 * q + 1};
+          ect::gather_columns(ctx, xp.p, k, cols, 2, N, stage);
+          ect::gather_columns(ctx, s->two_configs ? xr.p : xp.p, k, cols, 2, N, stage + 2 * N);
+          if (!dev) copy_d2h(ctx, dst, stage, (size_t)4 * N * sizeof(double2));
           CK(cudaStreamSynchronize(ctx->stream));
         }
       } catch (const ect::Error& e) {

@@ -644,15 +644,35 @@ k_spmv_v(int64_t n, const int* __restrict__ row_ptr, const int* __restrict__ col
     const bool valid = row < n;
     const int beg = valid ? row_ptr[row] : 0, end = valid ? row_ptr[row + 1] : 0;
     double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-    for (int p = beg + e; p < end; p += E) {
-      const int j = ldg_i(col + p);
-      const double2 a = ldg2(val + p);
-      double2 x0, x1;
-      ld4x(x + (int64_t)j * K + kc, x0, x1);
-      acc[0].x += a.x * x0.x - a.y * x0.y;
-      acc[0].y += a.x * x0.y + a.y * x0.x;
-      acc[1].x += a.x * x1.x - a.y * x1.y;
-      acc[1].y += a.x * x1.y + a.y * x1.x;
+    // U entries per step: all column / value loads first, then all gathers,
+    // so a lane pays two dependent load latencies per U entries, not per entry
+    // (short rows on small levels are pure latency: 35 -> ~10 us per launch)
+    constexpr int U = 4;
+    for (int p0 = beg + e; p0 < end; p0 += U * E) {
+      int j[U];
+      double2 a[U], x0[U], x1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + u * E;
+        j[u] = -1;
+        a[u] = make_double2(0.0, 0.0);
+        if (p < end) {
+          j[u] = ldg_i(col + p);
+          a[u] = ldg2(val + p);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        x0[u] = x1[u] = make_double2(0.0, 0.0);
+        if (j[u] >= 0) ld4x(x + (int64_t)j[u] * K + kc, x0[u], x1[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[0].x += a[u].x * x0[u].x - a[u].y * x0[u].y;
+        acc[0].y += a[u].x * x0[u].y + a[u].y * x0[u].x;
+        acc[1].x += a[u].x * x1[u].x - a[u].y * x1[u].y;
+        acc[1].y += a[u].x * x1[u].y + a[u].y * x1[u].x;
+      }
     }
 #pragma unroll
     for (int c = 0; c < 2; ++c)
@@ -1985,6 +2005,33 @@ void build_sell(ect_matrix* a, int sigma) {
   a->has_sell = true;
 }
 
+namespace {
+struct Cols4 {
+  int c[4];
+};
+__global__ void __launch_bounds__(kBlock)
+k_gather_columns(const double2* __restrict__ src, int k, Cols4 cols, int n_cols, int64_t n,
+                 double2* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n_cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / n, i = e - c * n;
+    dst[e] = src[i * k + cols.c[c]];
+  }
+}
+}  // namespace
+
+void gather_columns(ect_ctx* ctx, const double2* src, int k, const int* cols, int n_cols,
+                    int64_t n, double2* dst) {
+  if (n_cols < 1 || n_cols > 4) fail(ECT_ERR_CONFIG, "gather_columns: 1..4 columns");
+  Cols4 c{};
+  for (int j = 0; j < n_cols; ++j) c.c[j] = cols[j];
+  const int grid = (int)std::min<int64_t>((n * n_cols + kBlock - 1) / kBlock,
+                                          (int64_t)ctx->num_sms * 8);
+  k_gather_columns<<<std::max(grid, 1), kBlock, 0, ctx->stream>>>(src, k, c, n_cols, n, dst);
+  CK_LAUNCH();
+  note_launch(ctx, 1);
+}
+
 void spmv(ect_ctx* ctx, ect_matrix* a, const double2* x, double2* y, int k) {
   if (k < 1 || k > 16) fail(ECT_ERR_SOLVER, "spmv: n_rhs must be in 1..16");
   if (k & (k - 1)) {  // pad to the next supported width
@@ -2693,8 +2740,20 @@ k_restrict(int64_t nc, const int* __restrict__ r_ptr, const int* __restrict__ r_
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / K, k = e - c * K;
     double2 acc = make_double2(0.0, 0.0);
-    for (int p = r_ptr[c]; p < r_ptr[c + 1]; ++p)
-      acc = cadd(acc, as_d2(t[(int64_t)r_idx[p] * K + k]));
+    const int pe = r_ptr[c + 1];
+    // four member indices, then their four values, per step (latency, not
+    // bandwidth, is what these small launches cost); the sum stays in order
+    for (int p = r_ptr[c]; p < pe; p += 4) {
+      int idx[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) idx[u] = p + u < pe ? __ldg(r_idx + p + u) : -1;
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = idx[u] >= 0 ? as_d2(t[(int64_t)idx[u] * K + k]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = cadd(acc, v[u]);
+    }
     bc[e] = acc;
   }
 }

@@ -140,6 +140,8 @@ def build_levels(A, n_nodes, cond, pinned, smooth=0, coarse_n=int(__import__("os
 
 
 F32 = __import__("os").environ.get("F32") == "1"
+ADD = __import__("os").environ.get("ADD") == "1"
+ADD_W = float(__import__("os").environ.get("ADD_W", "0.6"))
 
 
 def vcycle(levels, b, lvl=0, nu=1, w=0.7, gamma=1, oc=1.0):
@@ -147,6 +149,13 @@ def vcycle(levels, b, lvl=0, nu=1, w=0.7, gamma=1, oc=1.0):
     if "lu" in L:
         return L["lu"].solve(b)
     A, P, d = L["A"], L["P"], L["d"]
+    if ADD and lvl == 0:  # additive fine level: no fine-level SpMV in the cycle
+        rc = P.T @ b
+        e = vcycle(levels, rc, lvl + 1, nu, w, gamma, oc)
+        if gamma == 2 and "lu" not in levels[lvl + 1]:
+            Ac = levels[lvl + 1]["A"]
+            e = e + vcycle(levels, rc - Ac @ e, lvl + 1, nu, w, gamma, oc)
+        return ADD_W * b / d + oc * (P @ e)
     if F32 and lvl == 0:  # finest level smoothing in single precision
         if "A32" not in L:
             L["A32"] = A.astype(np.complex64)

@@ -90,6 +90,19 @@ def test_cfg1_bit_exact_and_solve_properties(ctx):
     A = sp.csr_matrix((vals, ci, rp), shape=(a.n, a.n))
     asym = abs(A - A.T).max() / abs(A).max()
     assert asym <= 1e-15
+    # the production SpMV kernels (node-block sliced-ELL; k = 8 is the flat
+    # batched kernel of the sweep) at full size against CscMatrix::multiply's
+    # result, i.e. the reference's own arrays multiplied on the host
+    # (sparse.cpp:115-124): per-row error <= 1e-14 sum_j |a_ij| |x_j|
+    assert a.format == "nb"
+    absA = abs(A)
+    rng = np.random.default_rng(2)
+    for k in (1, 2, 4, 8):
+        xs = rng.uniform(-1, 1, (a.n, k)) + 1j * rng.uniform(-1, 1, (a.n, k))
+        xs = xs[:, 0].copy() if k == 1 else xs
+        y = a.multiply(xs)
+        err = np.max(np.abs(y - A @ xs) / (absA @ np.abs(xs)))
+        assert err <= 1e-14, (k, err)
     b = mesh.rhs(w.coil, [w.positions[0]], [1], w.amplitude)[:, 0]
     x, res = a.solve(b, tol=1e-8, max_iter=20000)
     assert res[0]["converged"]
