@@ -228,7 +228,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         e2e = e2e_leg(ect, ctx, sess, mesh, w, positions, max(1, args.steps), rank, world, ppb,
-                      step_positions)
+                      step_positions, first_step=args.warmup)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -316,7 +316,8 @@ def rank_info(local, world):
     return out
 
 
-def e2e_leg(ect, ctx, sess, mesh, w, positions, steps, rank, world, ppb, step_positions):
+def e2e_leg(ect, ctx, sess, mesh, w, positions, steps, rank, world, ppb, step_positions,
+            first_step=0):
     """Same metric through the public ABI with host buffers (pinned).
 
     Headline: ect_session_solve_positions (ScanSession::solve_position) with the
@@ -334,8 +335,9 @@ def e2e_leg(ect, ctx, sess, mesh, w, positions, steps, rank, world, ppb, step_po
         import torch.distributed as dist
         dist.barrier()
     t0 = time.perf_counter()
-    for s in range(steps):
-        pts = sess.solve_positions(step_positions(s), positions_per_batch=ppb, solutions=sol)
+    for s in range(steps):  # the same probe positions as the device-timed steps
+        pts = sess.solve_positions(step_positions(first_step + s), positions_per_batch=ppb,
+                                   solutions=sol)
         iters_s += sum(sum(p["iterations"]) for p in pts)
     dt_s = time.perf_counter() - t0
     dt_max, it_all, _, _ = sharding.reduce_timing(dt_s * 1e3, float(iters_s), 0, 0,

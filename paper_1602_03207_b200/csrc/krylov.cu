@@ -188,7 +188,34 @@ struct KrylovCtl {
   // kSmoothDot: 1 = first preconditioned residual of a (re)start (sets rho),
   // 0 = an iteration (beta = rho_new / rho)
   int rho_start;
+  // dev (ECT_TRACE_SOLVE=1): relative recurrence residual per iteration,
+  // hist[iters * hist_k + column], iterations < hist_cap
+  double* hist = nullptr;
+  int hist_cap = 0, hist_k = 0;
 };
+__device__ __forceinline__ void trace_residual(const KrylovCtl& ctl, const RhsState& s, int k) {
+  if (ctl.hist && s.iters < ctl.hist_cap)
+    ctl.hist[(size_t)s.iters * ctl.hist_k + k] = s.bnorm > 0.0 ? s.rnorm / s.bnorm : 0.0;
+}
+
+// COCG has no look-ahead: a near-breakdown (p^T A p ~ 0) makes one huge step
+// that throws the residual up by orders of magnitude, after which the
+// recurrence no longer recovers (measured on configs[1] at tol 1e-12: 7e-11 ->
+// 5e-7 in one step, then stagnation near 1e-7). The iteration's x += alpha p is
+// still owed when the update's last block sees the new norm, so such a step
+// can be taken back exactly: alpha -> 0 (x keeps its value), k_undo restores
+// r += alpha q, and the next direction is p = z (beta = 0). Not twice in a row.
+constexpr double kSpike = 100.0;  // ||r_new|| / best ||r|| since the last (re)start
+__device__ __forceinline__ bool take_back(const KrylovCtl& ctl, RhsState& s, double r_prev) {
+  if (ctl.red) return false;  // partitioned solve: its loop has no k_undo
+  if (!(s.rnorm > kSpike * s.rbest) || s.undo_iter == (double)(s.iters - 1)) return false;
+  s.omega = s.alpha;  // kept for k_undo (omega is BiCGStab's, unused by COCG)
+  s.alpha = make_double2(0.0, 0.0);
+  s.rnorm = r_prev;
+  s.undo = 1;
+  s.undo_iter = (double)s.iters;
+  return true;
+}
 
 // ---- scalar finalisations (run by one thread on the global totals) ----------
 template <int K>
@@ -224,12 +251,18 @@ __device__ void fin_update(const KrylovCtl& ctl, const double* tot) {
     s.xpend = s.status == kActive;  // this iteration's x += alpha p is owed to k_pupdate
     if (s.status != kActive) continue;
     const double2 rho_new = make_double2(tot[3 * k], tot[3 * k + 1]);
+    const double r_prev = s.rnorm;
     s.rnorm = sqrt(tot[3 * k + 2]);
     s.iters += 1;
+    trace_residual(ctl, s, k);
+    if (s.rnorm < s.rbest) s.rbest = s.rnorm;
     if (s.rnorm <= ctl.tol * s.bnorm) {
       s.status = kConverged;
     } else if (s.iters >= ctl.max_iter) {
       s.status = kMaxIter;
+    } else if (take_back(ctl, s, r_prev)) {
+      s.beta = make_double2(0.0, 0.0);  // p = z: the direction restarts from r
+      ++active;
     } else if (rho_new.x == 0.0 && rho_new.y == 0.0) {
       s.status = kBreakdown;
     } else {
@@ -252,13 +285,17 @@ __device__ void fin_update_norm(const KrylovCtl& ctl, const double* tot) {
     RhsState& s = ctl.st[k];
     s.xpend = s.status == kActive;
     if (s.status != kActive) continue;
+    const double r_prev = s.rnorm;
     s.rnorm = sqrt(tot[k]);
     s.iters += 1;
+    trace_residual(ctl, s, k);
+    if (s.rnorm < s.rbest) s.rbest = s.rnorm;
     if (s.rnorm <= ctl.tol * s.bnorm) {
       s.status = kConverged;
     } else if (s.iters >= ctl.max_iter) {
       s.status = kMaxIter;
     } else {
+      take_back(ctl, s, r_prev);
       ++active;
     }
   }
@@ -278,6 +315,10 @@ __device__ void fin_rho(const KrylovCtl& ctl, const double* tot) {
       continue;
     }
     if (!ctl.rho_start) s.beta = cdiv(rho_new, s.rho);
+    if (s.undo) {  // the step was taken back: p = z, the direction restarts from r
+      s.beta = make_double2(0.0, 0.0);
+      s.undo = 0;
+    }
     s.rho = rho_new;
     ++active;
   }
@@ -296,7 +337,9 @@ __device__ void fin_start_norm(const KrylovCtl& ctl, const double* tot, unsigned
         s.bnorm = sqrt(tot[2 * k + 1]);
         s.iters = 0;
       }
-      s.rnorm = sqrt(tot[2 * k]);
+      s.rnorm = s.rbest = sqrt(tot[2 * k]);
+      s.undo = 0;
+      s.undo_iter = -1.0;
       if (fresh && s.bnorm == 0.0) s.status = kZeroRhs;
       else if (s.rnorm <= ctl.tol * s.bnorm) s.status = kConverged;
       else s.status = kActive;
@@ -318,7 +361,9 @@ __device__ void fin_start(const KrylovCtl& ctl, const double* tot, unsigned mask
         s.iters = 0;
       }
       s.rho = make_double2(tot[4 * k], tot[4 * k + 1]);
-      s.rnorm = sqrt(tot[4 * k + 2]);
+      s.rnorm = s.rbest = sqrt(tot[4 * k + 2]);
+      s.undo = 0;
+      s.undo_iter = -1.0;
       if (fresh && s.bnorm == 0.0) {
         s.status = kZeroRhs;
       } else if (s.rnorm <= ctl.tol * s.bnorm) {
@@ -1460,6 +1505,54 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
   }
 }
 
+// Takes back the update of flagged columns (RhsState::undo, see take_back):
+// r += alpha q with the alpha the update used, and the multigrid cycle's
+// pre-smoothing iterate recomputed from the restored r. Early exit otherwise.
+// JACOBI: nothing downstream consumes the flag (beta is already 0): clear it.
+template <int K, bool JACOBI>
+__global__ void __launch_bounds__(kBlock)
+k_undo(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
+       const double2* __restrict__ dinv, KrylovCtl ctl, double2* __restrict__ xt, double omega,
+       float2* __restrict__ xt32) {
+  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < K; ++c) any |= ctl.st[c].undo != 0 && ctl.st[c].status == kActive;
+  if (!any) return;
+  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
+  bool on[CW];
+  double2 alpha[CW];
+#pragma unroll
+  for (int c = 0; c < CW; ++c) {
+    on[c] = ctl.st[kb + c].undo != 0 && ctl.st[kb + c].status == kActive;
+    alpha[c] = ctl.st[kb + c].omega;
+  }
+  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / KH;
+    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);
+    const double2 d = dinv[i];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) {
+      if (!on[c]) continue;
+      const int64_t idx = i * K + kb + c;
+      const double2 rv = cadd(r[idx], cmul(alpha[c], q[idx]));
+      r[idx] = rv;
+      if (xt) xt[idx] = cmul(make_double2(omega * d.x, omega * d.y), rv);
+      if (xt32) put(xt32 + idx, cmul(make_double2(omega * d.x, omega * d.y), rv));
+    }
+  }
+  if constexpr (JACOBI) {
+    if (!last_block(ctl.counter)) return;
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) ctl.st[c].undo = 0;
+      *ctl.counter = 0u;
+    }
+  }
+}
+
 // x += alpha p (owed by the last k_update) ; p = z + beta p (active columns),
 // z = D^-1 r (Jacobi) or the preconditioner's output zv (EXT)
 template <int K, bool EXT = false>
@@ -2160,6 +2253,7 @@ k_bi_dot(int64_t n, const double2* __restrict__ a, const double2* __restrict__ b
 }
 
 constexpr double kBiGrowth = 1e4;  // recurrence residual / best since restart -> restart
+constexpr int kBiReplace = 48;     // iterations between residual replacements
 
 // x += alpha p_hat + omega s_hat ; r = s - omega t ; rho_new = (r_hat, r), ||r||
 template <int K>
@@ -2324,7 +2418,7 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
   int* flag = ctx->pinned_flag;
   const int chunk = 16;
   for (int restart_round = 0;; ++restart_round) {
-    int polls = 0, launched = 0;
+    int polls = 0, launched = 0, since_replace = 0;
     cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
     const int cap = opt.max_iter + chunk;
     for (; opt.max_iter > 0;) {
@@ -2338,6 +2432,17 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
         k_bi_x<K><<<grid_v, kBlock, 0, s>>>(n, W.xx.p, W.r.p, W.ph.p, W.sh.p, W.t.p, W.rh.p, ctl);
         CK_LAUNCH();
         note_launch(ctx, 7);
+        // residual replacement: every kBiReplace iterations r <- b - A x (p, v
+        // and the scalars are kept), so the recurrence residual cannot drift
+        // away from the true one while the iteration is still far from the
+        // tolerance; without it the tight-tolerance solves of the impedance
+        // fixture converge in the recurrence at a true residual of 1e-10 and
+        // restart from scratch again and again
+        if (++since_replace == kBiReplace) {
+          DK::spmv(ctx, kResid, grid_r, n, a, W.xx.p, W.r.p, W.bb.p, ctl);
+          note_launch(ctx, 1);
+          since_replace = 0;
+        }
       }
       launched += chunk;
       CK(cudaMemcpyAsync(flag + (polls & 1), W.n_active.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -3105,6 +3210,15 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
     }
     KrylovCtl ctl{st.p, n_active.p, counter.p, partial.p, opt.tol, opt.max_iter,
                   nullptr, 0, n, n, n};
+    DevBuf<double> hist;
+    const bool trace = std::getenv("ECT_TRACE_SOLVE") != nullptr;
+    if (trace) {
+      ctl.hist_cap = std::min(opt.max_iter + 1, 1 << 16);
+      ctl.hist_k = kk;
+      hist.alloc((size_t)ctl.hist_cap * kk);
+      CK(cudaMemsetAsync(hist.p, 0, hist.bytes(), s));
+      ctl.hist = hist.p;
+    }
     const unsigned all = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
     // (re)start: norms (+ p = D^-1 r, rho with Jacobi); multigrid then sets
     // p = M r and rho = r^T M r
@@ -3148,6 +3262,10 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
                 n, r.p, q.p, a->dinv.p, ctl, fuse && !cyc->f32 ? a->amg->lv[0].xt.p : nullptr,
                 a->amg->omega, fuse && cyc->f32 ? a->amg->xt32.p : nullptr);
             CK_LAUNCH();
+            k_undo<KW, false><<<grid_v, kBlock, 0, s>>>(
+                n, r.p, q.p, a->dinv.p, ctl, fuse && !cyc->f32 ? a->amg->lv[0].xt.p : nullptr,
+                a->amg->omega, fuse && cyc->f32 ? a->amg->xt32.p : nullptr);
+            CK_LAUNCH();
             prof_end(ctx, ev2);
             cudaEvent_t ev3[2];
             ev3[0] = ev3[1] = nullptr;
@@ -3158,10 +3276,13 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
             CK_LAUNCH();
           } else {
             DK::update(ctx, grid_v, n, r.p, q.p, a->dinv.p, ctl);
+            k_undo<KW, true><<<grid_v, kBlock, 0, s>>>(n, r.p, q.p, a->dinv.p, ctl, nullptr, 0.0,
+                                                      nullptr);
+            CK_LAUNCH();
             DK::pupdate(ctx, grid_v, n, xx.p, r.p, p.p, a->dinv.p, ctl);
             prof_end(ctx, ev2);
           }
-          note_launch(ctx, 3);
+          note_launch(ctx, 4);
         }
         launched += chunk;
         CK(cudaMemcpyAsync(flag + (polls_in_flight & 1), n_active.p, sizeof(int),
@@ -3215,6 +3336,17 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
       start(restart_mask, 0);
       // keep the other columns frozen
       CK(cudaStreamSynchronize(s));
+    }
+    if (trace) {  // dev: recurrence residual history, every 10th iteration
+      std::vector<double> h((size_t)ctl.hist_cap * kk);
+      CK(cudaMemcpy(h.data(), hist.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int c = 0; c < k; ++c) {
+        std::fprintf(stderr, "[ect trace] column %d (iterations %d, true %.3e):", c, hs[c].iters,
+                     hs[c].bnorm > 0.0 ? hs[c].rnorm / hs[c].bnorm : 0.0);
+        for (int it = 1; it <= hs[c].iters && it < ctl.hist_cap; it += (it < 20 ? 1 : 10))
+          std::fprintf(stderr, " %d:%.2e", it, h[(size_t)it * kk + c]);
+        std::fprintf(stderr, "\n");
+      }
     }
     for (int c = 0; c < k; ++c) {
       const RhsState& t = hs[c];
