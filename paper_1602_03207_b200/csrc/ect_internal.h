@@ -74,9 +74,9 @@ struct RhsState {
   int iters;
   int status;     // kActive / kConverged / kBreakdown / kMaxIter / kZeroRhs
   int xpend;      // COCG: x += alpha p still owed (applied by the next p-update)
-  int undo;       // COCG: the last step blew the residual up and is being taken back
-  double rbest;   // smallest recurrence residual since the last (re)start
-  double undo_iter;  // COCG: iteration of the last step taken back
+  int restart_dir;  // COCG: stalled, the next direction is p = z (beta = 0)
+  double rbest;     // smallest recurrence residual since the last (re)start
+  double best_iter; // iteration that set rbest
 };
 enum RhsStatus : int { kActive = 0, kConverged = 1, kBreakdown = 2, kMaxIter = 3, kZeroRhs = 4 };
 

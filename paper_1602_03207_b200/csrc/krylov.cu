@@ -198,23 +198,28 @@ __device__ __forceinline__ void trace_residual(const KrylovCtl& ctl, const RhsSt
     ctl.hist[(size_t)s.iters * ctl.hist_k + k] = s.bnorm > 0.0 ? s.rnorm / s.bnorm : 0.0;
 }
 
-// COCG has no look-ahead: a near-breakdown (p^T A p ~ 0) makes one huge step
-// that throws the residual up by orders of magnitude, after which the
-// recurrence no longer recovers (measured on configs[1] at tol 1e-12: 7e-11 ->
-// 5e-7 in one step, then stagnation near 1e-7). The iteration's x += alpha p is
-// still owed when the update's last block sees the new norm, so such a step
-// can be taken back exactly: alpha -> 0 (x keeps its value), k_undo restores
-// r += alpha q, and the next direction is p = z (beta = 0). Not twice in a row.
-constexpr double kSpike = 100.0;  // ||r_new|| / best ||r|| since the last (re)start
-__device__ __forceinline__ bool take_back(const KrylovCtl& ctl, RhsState& s, double r_prev) {
-  if (ctl.red) return false;  // partitioned solve: its loop has no k_undo
-  if (!(s.rnorm > kSpike * s.rbest) || s.undo_iter == (double)(s.iters - 1)) return false;
-  s.omega = s.alpha;  // kept for k_undo (omega is BiCGStab's, unused by COCG)
-  s.alpha = make_double2(0.0, 0.0);
-  s.rnorm = r_prev;
-  s.undo = 1;
-  s.undo_iter = (double)s.iters;
-  return true;
+// COCG has no look-ahead: after a near-breakdown (p^T A p ~ 0: one huge step,
+// the residual jumps by orders of magnitude) the recurrences stop producing
+// conjugate directions and the residual hovers instead of converging (measured
+// on configs[1] at tol 1e-12: 7e-11 at iteration 90, 5e-7 at 110, then ~1e-7
+// for 300 iterations), although a fresh start from the same residual converges
+// at the initial rate. With the multigrid preconditioner a healthy solve sets a
+// new best residual at least every ~30 iterations, so a column that has not
+// improved for kStall iterations restarts its direction: p = z (beta = 0), the
+// window and the best value are reset, x and r are untouched. (Taking the big
+// step back instead was tried and is worse: COCG's route to convergence goes
+// through 10-100x peaks, and restarting at each one forfeits the superlinear
+// phase.)
+constexpr int kStall = 50;
+__device__ __forceinline__ void stall_check(RhsState& s) {
+  if (s.rnorm < s.rbest) {
+    s.rbest = s.rnorm;
+    s.best_iter = (double)s.iters;
+  } else if ((double)s.iters - s.best_iter >= (double)kStall) {
+    s.restart_dir = 1;  // consumed by fin_rho
+    s.rbest = s.rnorm;
+    s.best_iter = (double)s.iters;
+  }
 }
 
 // ---- scalar finalisations (run by one thread on the global totals) ----------
@@ -251,18 +256,13 @@ __device__ void fin_update(const KrylovCtl& ctl, const double* tot) {
     s.xpend = s.status == kActive;  // this iteration's x += alpha p is owed to k_pupdate
     if (s.status != kActive) continue;
     const double2 rho_new = make_double2(tot[3 * k], tot[3 * k + 1]);
-    const double r_prev = s.rnorm;
     s.rnorm = sqrt(tot[3 * k + 2]);
     s.iters += 1;
     trace_residual(ctl, s, k);
-    if (s.rnorm < s.rbest) s.rbest = s.rnorm;
     if (s.rnorm <= ctl.tol * s.bnorm) {
       s.status = kConverged;
     } else if (s.iters >= ctl.max_iter) {
       s.status = kMaxIter;
-    } else if (take_back(ctl, s, r_prev)) {
-      s.beta = make_double2(0.0, 0.0);  // p = z: the direction restarts from r
-      ++active;
     } else if (rho_new.x == 0.0 && rho_new.y == 0.0) {
       s.status = kBreakdown;
     } else {
@@ -285,17 +285,15 @@ __device__ void fin_update_norm(const KrylovCtl& ctl, const double* tot) {
     RhsState& s = ctl.st[k];
     s.xpend = s.status == kActive;
     if (s.status != kActive) continue;
-    const double r_prev = s.rnorm;
     s.rnorm = sqrt(tot[k]);
     s.iters += 1;
     trace_residual(ctl, s, k);
-    if (s.rnorm < s.rbest) s.rbest = s.rnorm;
     if (s.rnorm <= ctl.tol * s.bnorm) {
       s.status = kConverged;
     } else if (s.iters >= ctl.max_iter) {
       s.status = kMaxIter;
     } else {
-      take_back(ctl, s, r_prev);
+      stall_check(s);
       ++active;
     }
   }
@@ -315,9 +313,9 @@ __device__ void fin_rho(const KrylovCtl& ctl, const double* tot) {
       continue;
     }
     if (!ctl.rho_start) s.beta = cdiv(rho_new, s.rho);
-    if (s.undo) {  // the step was taken back: p = z, the direction restarts from r
+    if (s.restart_dir) {  // stalled (stall_check): p = z, the direction restarts from r
       s.beta = make_double2(0.0, 0.0);
-      s.undo = 0;
+      s.restart_dir = 0;
     }
     s.rho = rho_new;
     ++active;
@@ -338,8 +336,8 @@ __device__ void fin_start_norm(const KrylovCtl& ctl, const double* tot, unsigned
         s.iters = 0;
       }
       s.rnorm = s.rbest = sqrt(tot[2 * k]);
-      s.undo = 0;
-      s.undo_iter = -1.0;
+      s.restart_dir = 0;
+      s.best_iter = (double)s.iters;
       if (fresh && s.bnorm == 0.0) s.status = kZeroRhs;
       else if (s.rnorm <= ctl.tol * s.bnorm) s.status = kConverged;
       else s.status = kActive;
@@ -362,8 +360,8 @@ __device__ void fin_start(const KrylovCtl& ctl, const double* tot, unsigned mask
       }
       s.rho = make_double2(tot[4 * k], tot[4 * k + 1]);
       s.rnorm = s.rbest = sqrt(tot[4 * k + 2]);
-      s.undo = 0;
-      s.undo_iter = -1.0;
+      s.restart_dir = 0;
+      s.best_iter = (double)s.iters;
       if (fresh && s.bnorm == 0.0) {
         s.status = kZeroRhs;
       } else if (s.rnorm <= ctl.tol * s.bnorm) {
@@ -1505,54 +1503,6 @@ k_update(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
   }
 }
 
-// Takes back the update of flagged columns (RhsState::undo, see take_back):
-// r += alpha q with the alpha the update used, and the multigrid cycle's
-// pre-smoothing iterate recomputed from the restored r. Early exit otherwise.
-// JACOBI: nothing downstream consumes the flag (beta is already 0): clear it.
-template <int K, bool JACOBI>
-__global__ void __launch_bounds__(kBlock)
-k_undo(int64_t n, double2* __restrict__ r, const double2* __restrict__ q,
-       const double2* __restrict__ dinv, KrylovCtl ctl, double2* __restrict__ xt, double omega,
-       float2* __restrict__ xt32) {
-  constexpr int CW = VecMap<K>::CW, KH = VecMap<K>::KH;
-  bool any = false;
-#pragma unroll
-  for (int c = 0; c < K; ++c) any |= ctl.st[c].undo != 0 && ctl.st[c].status == kActive;
-  if (!any) return;
-  const int h = (threadIdx.x & 31) % KH, kb = h * CW;
-  bool on[CW];
-  double2 alpha[CW];
-#pragma unroll
-  for (int c = 0; c < CW; ++c) {
-    on[c] = ctl.st[kb + c].undo != 0 && ctl.st[kb + c].status == kActive;
-    alpha[c] = ctl.st[kb + c].omega;
-  }
-  const int64_t len0 = ctl.e0 - ctl.s0, rows = len0 + (ctl.e1 - ctl.s1);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * KH;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / KH;
-    const int64_t i = j < len0 ? ctl.s0 + j : ctl.s1 + (j - len0);
-    const double2 d = dinv[i];
-#pragma unroll
-    for (int c = 0; c < CW; ++c) {
-      if (!on[c]) continue;
-      const int64_t idx = i * K + kb + c;
-      const double2 rv = cadd(r[idx], cmul(alpha[c], q[idx]));
-      r[idx] = rv;
-      if (xt) xt[idx] = cmul(make_double2(omega * d.x, omega * d.y), rv);
-      if (xt32) put(xt32 + idx, cmul(make_double2(omega * d.x, omega * d.y), rv));
-    }
-  }
-  if constexpr (JACOBI) {
-    if (!last_block(ctl.counter)) return;
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int c = 0; c < K; ++c) ctl.st[c].undo = 0;
-      *ctl.counter = 0u;
-    }
-  }
-}
-
 // x += alpha p (owed by the last k_update) ; p = z + beta p (active columns),
 // z = D^-1 r (Jacobi) or the preconditioner's output zv (EXT)
 template <int K, bool EXT = false>
@@ -2253,7 +2203,7 @@ k_bi_dot(int64_t n, const double2* __restrict__ a, const double2* __restrict__ b
 }
 
 constexpr double kBiGrowth = 1e4;  // recurrence residual / best since restart -> restart
-constexpr int kBiReplace = 48;     // iterations between residual replacements
+constexpr int kBiStall = 600;      // iterations without a new best residual -> restart
 
 // x += alpha p_hat + omega s_hat ; r = s - omega t ; rho_new = (r_hat, r), ||r||
 template <int K>
@@ -2296,16 +2246,22 @@ k_bi_x(int64_t n, double2* __restrict__ x, double2* __restrict__ r,
       const double2 rho_new = make_double2(tot[NVL * c], tot[NVL * c + 1]);
       s.rnorm = sqrt(tot[NVL * c + 2]);
       s.iters += 1;
-      if (s.rnorm < s.rbest) s.rbest = s.rnorm;
+      if (s.rnorm < s.rbest) {
+        s.rbest = s.rnorm;
+        s.best_iter = (double)s.iters;
+      }
       if (s.rnorm <= ctl.tol * s.bnorm) {
         s.status = kConverged;
       } else if (s.iters >= ctl.max_iter) {
         s.status = kMaxIter;
       } else if ((rho_new.x == 0.0 && rho_new.y == 0.0) || (s.omega.x == 0.0 && s.omega.y == 0.0) ||
-                 !(s.rnorm <= kBiGrowth * s.rbest)) {
-        // Lanczos (near-)breakdown, or the recurrence residual has grown far
-        // above its best value (also NaN): restart from the true residual
-        // before the drift reaches x
+                 !(s.rnorm <= kBiGrowth * s.rbest) ||
+                 (double)s.iters - s.best_iter >= (double)kBiStall) {
+        // Lanczos (near-)breakdown; or the recurrence residual has grown far
+        // above its best value (also NaN); or it has not improved for kBiStall
+        // iterations (the recurrence has drifted from b - A x and hovers above
+        // the tolerance): restart from the true residual, which turns the
+        // solve into iterative refinement with BiCGStab as the inner solver
         s.status = kBreakdown;
       } else {
         s.beta = cmul(cdiv(rho_new, s.rho), cdiv(s.alpha, s.omega));
@@ -2365,6 +2321,7 @@ k_bi_start(int64_t n, const double2* __restrict__ b, double2* __restrict__ x,
           s.iters = 0;
         }
         s.rnorm = s.rbest = sqrt(rr);
+        s.best_iter = (double)s.iters;
         s.rho = make_double2(rr, 0.0);
         s.alpha = s.omega = make_double2(1.0, 0.0);
         s.beta = make_double2(0.0, 0.0);
@@ -2418,7 +2375,7 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
   int* flag = ctx->pinned_flag;
   const int chunk = 16;
   for (int restart_round = 0;; ++restart_round) {
-    int polls = 0, launched = 0, since_replace = 0;
+    int polls = 0, launched = 0;
     cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
     const int cap = opt.max_iter + chunk;
     for (; opt.max_iter > 0;) {
@@ -2432,17 +2389,6 @@ void bicgstab_k(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
         k_bi_x<K><<<grid_v, kBlock, 0, s>>>(n, W.xx.p, W.r.p, W.ph.p, W.sh.p, W.t.p, W.rh.p, ctl);
         CK_LAUNCH();
         note_launch(ctx, 7);
-        // residual replacement: every kBiReplace iterations r <- b - A x (p, v
-        // and the scalars are kept), so the recurrence residual cannot drift
-        // away from the true one while the iteration is still far from the
-        // tolerance; without it the tight-tolerance solves of the impedance
-        // fixture converge in the recurrence at a true residual of 1e-10 and
-        // restart from scratch again and again
-        if (++since_replace == kBiReplace) {
-          DK::spmv(ctx, kResid, grid_r, n, a, W.xx.p, W.r.p, W.bb.p, ctl);
-          note_launch(ctx, 1);
-          since_replace = 0;
-        }
       }
       launched += chunk;
       CK(cudaMemcpyAsync(flag + (polls & 1), W.n_active.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2961,6 +2907,7 @@ k_rho(int64_t n, const double2* __restrict__ r, const double2* __restrict__ z, K
   }
 }
 
+
 template <int K>
 struct Cycle {
   using DK = Dispatch<K>;
@@ -3262,10 +3209,6 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
                 n, r.p, q.p, a->dinv.p, ctl, fuse && !cyc->f32 ? a->amg->lv[0].xt.p : nullptr,
                 a->amg->omega, fuse && cyc->f32 ? a->amg->xt32.p : nullptr);
             CK_LAUNCH();
-            k_undo<KW, false><<<grid_v, kBlock, 0, s>>>(
-                n, r.p, q.p, a->dinv.p, ctl, fuse && !cyc->f32 ? a->amg->lv[0].xt.p : nullptr,
-                a->amg->omega, fuse && cyc->f32 ? a->amg->xt32.p : nullptr);
-            CK_LAUNCH();
             prof_end(ctx, ev2);
             cudaEvent_t ev3[2];
             ev3[0] = ev3[1] = nullptr;
@@ -3276,13 +3219,10 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
             CK_LAUNCH();
           } else {
             DK::update(ctx, grid_v, n, r.p, q.p, a->dinv.p, ctl);
-            k_undo<KW, true><<<grid_v, kBlock, 0, s>>>(n, r.p, q.p, a->dinv.p, ctl, nullptr, 0.0,
-                                                      nullptr);
-            CK_LAUNCH();
             DK::pupdate(ctx, grid_v, n, xx.p, r.p, p.p, a->dinv.p, ctl);
             prof_end(ctx, ev2);
           }
-          note_launch(ctx, 4);
+          note_launch(ctx, 3);
         }
         launched += chunk;
         CK(cudaMemcpyAsync(flag + (polls_in_flight & 1), n_active.p, sizeof(int),
