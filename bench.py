@@ -101,25 +101,47 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        # ONE long-lived nvidia-smi in loop mode (NVML initialised once): a fresh
+        # nvidia-smi process every sample takes driver locks for tens of ms each
+        # and showed up as outliers in sub-second timed regions
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "250"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._proc = None
+            return
+        for line in self._proc.stdout:
+            line = line.strip()
+            if line:
+                self.samples.append([v.strip() for v in line.split(",")])
+            if self._stop.is_set():
+                break
 
     def __enter__(self):
+        self._proc = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
+        if self._proc is not None:
+            try:
+                self._proc.terminate()
+            except Exception:
+                pass
         self._t.join(timeout=10)
+        if not self.samples:  # region shorter than one loop period: one direct sample
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:

@@ -205,8 +205,12 @@ __device__ __forceinline__ void trace_residual(const KrylovCtl& ctl, const RhsSt
 // for 300 iterations), although a fresh start from the same residual converges
 // at the initial rate. With the multigrid preconditioner a healthy solve sets a
 // new best residual at least every ~30 iterations, so a column that has not
-// improved for kStall iterations restarts its direction: p = z (beta = 0), the
-// window and the best value are reset, x and r are untouched. (Taking the big
+// improved for max(kStall, iterations / 2) iterations restarts its direction:
+// p = z (beta = 0), the window and the best value are reset, x and r are
+// untouched. The window grows with the iteration count because a slow, noisy
+// but converging solve (multigrid on a matrix given without its mesh: 500-2000
+// iterations) goes 300 iterations between best values late in the solve; a
+// fixed 50-iteration window restarts it to death (measured). (Taking the big
 // step back instead was tried and is worse: COCG's route to convergence goes
 // through 10-100x peaks, and restarting at each one forfeits the superlinear
 // phase.)
@@ -215,7 +219,7 @@ __device__ __forceinline__ void stall_check(RhsState& s) {
   if (s.rnorm < s.rbest) {
     s.rbest = s.rnorm;
     s.best_iter = (double)s.iters;
-  } else if ((double)s.iters - s.best_iter >= (double)kStall) {
+  } else if ((double)s.iters - s.best_iter >= fmax((double)kStall, 0.5 * (double)s.iters)) {
     s.restart_dir = 1;  // consumed by fin_rho
     s.rbest = s.rnorm;
     s.best_iter = (double)s.iters;

@@ -1,6 +1,6 @@
 # round-end style GPU pass: tests, bench lines, launch list, ncu captures (one GPU)
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
+[ -n "$SKIP_TESTS" ] || { python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log; }
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
