@@ -107,7 +107,25 @@ struct AmgLevel {
   DevBuf<int> r_ptr, r_idx;          // coarse dof -> its dofs, ascending
   DevBuf<double2> xt, t, b, out, b2, out2;  // cycle work vectors [n][kcap]
 };
+// One solver iteration captured as a CUDA graph, kept with the hierarchy it
+// replays; valid while the batch width, the solver workspace and the stopping
+// parameters baked into the kernel arguments are unchanged.
+struct IterGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0, k = 0, max_iter = 0;
+  double tol = 0.0;
+  const void* tag[3] = {nullptr, nullptr, nullptr};
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+  }
+  ~IterGraph() { reset(); }
+};
 struct Amg {
+  IterGraph iter;
   std::vector<AmgLevel> lv;          // lv.back() is the dense coarsest level
   DevBuf<double2> minv;              // [n][n] row-major inverse of the coarsest matrix
   double omega = 0.6;                // damped-Jacobi weight
@@ -140,6 +158,8 @@ struct ect_ctx {
   int* pinned_flag = nullptr;  // small pinned word for convergence polling
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // convergence polling (krylov.cu)
   cudaEvent_t marks[8] = {};                    // ect_ctx_mark / ect_ctx_elapsed_ms
+  std::vector<cudaEvent_t> timer_events;        // EventTimer pool (2 per nesting level)
+  int timer_depth = 0;
   cudaStream_t halo_stream = nullptr;           // distributed solve: halo exchange
   cudaEvent_t ev_h1 = nullptr, ev_h2 = nullptr;
   bool force_csr = false;                       // ect_ctx_set_format(ctx, ECT_FORMAT_CSR)
@@ -172,6 +192,12 @@ struct ect_mesh {
   ect::DevBuf<int> nbr;            // neighbour node ids ascending, incl. self
   ect::DevBuf<uint8_t> nbr_cond;   // neighbour shares a conductor tet
   bool have_nbr = false;
+  // scratch of the per-position kernels (right-hand sides, impedance), kept
+  // across calls: cudaMalloc / cudaFree take driver-wide locks and synchronise
+  // the device, which showed up as sporadic 0.3-1.3 s stalls per sweep step
+  ect::DevBuf<uint8_t> rhs_flag;
+  ect::DevBuf<double> rhs_j, dz_contrib, dz_res;
+  ect::DevBuf<int> rhs_stat;
   // host copies (host-side reference semantics: mu_tilde, z extremes)
   std::vector<double> h_xyz;
   std::vector<int32_t> h_tets;

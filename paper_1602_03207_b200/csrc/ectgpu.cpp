@@ -178,13 +178,20 @@ struct ScopedDevice {
 };
 
 // Device-time accounting of one phase with its own event pair.
-struct EventTimer {
+struct EventTimer {  // events come from a per-context pool (created once, reused)
   ect_ctx* ctx;
   double* slot;
   cudaEvent_t a = nullptr, b = nullptr;
   EventTimer(ect_ctx* c, double* s) : ctx(c), slot(s) {
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
+    auto& pool = ctx->timer_events;
+    const size_t at = 2 * (size_t)ctx->timer_depth++;
+    while (pool.size() < at + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    a = pool[at];
+    b = pool[at + 1];
     CK(cudaEventRecord(a, ctx->stream));
   }
   ~EventTimer() {
@@ -192,8 +199,7 @@ struct EventTimer {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) *slot += ms;
     }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    --ctx->timer_depth;
   }
 };
 
@@ -293,6 +299,7 @@ int ect_ctx_destroy(ect_ctx* ctx) {
     ScopedDevice sd(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
+    for (auto e : ctx->timer_events) cudaEventDestroy(e);
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto e : ctx->stage_ev)

@@ -1815,16 +1815,23 @@ void with_k(int k, F&& fn) {
 // sampled = true (solver loop): time one launch in kProfStride, so the event
 // records do not perturb the timed region; the mean is over the sampled ones.
 constexpr int kProfStride = 8;
+int prof_stride() {
+  static const int stride = [] {
+    const char* v = std::getenv("ECT_PROF_STRIDE");  // dev: sample every n-th iteration
+    return v ? std::max(1, std::atoi(v)) : kProfStride;
+  }();
+  return stride;
+}
+// true when the next solver iteration is one of the profiled samples
+bool prof_sample_next(ect_ctx* ctx) {
+  return ctx->prof.enabled && (ctx->prof.launches % prof_stride()) == 0;
+}
 void prof_begin(ect_ctx* ctx, cudaEvent_t* ev, int kind = 0, bool sampled = false,
                 const int* n_active = nullptr, int width = 0, int snap = -1) {
   ev[0] = ev[1] = nullptr;
   if (!ctx->prof.enabled) return;
   auto& P = ctx->prof;
-  static const int stride = [] {
-    const char* v = std::getenv("ECT_PROF_STRIDE");  // dev: sample every n-th iteration
-    return v ? std::max(1, std::atoi(v)) : kProfStride;
-  }();
-  if (sampled && (P.launches++ % stride) != 0) return;
+  if (sampled && (P.launches++ % prof_stride()) != 0) return;
   if (P.used + 2 > P.pool.size()) {
     for (int i = 0; i < 512; ++i) {
       cudaEvent_t e;
@@ -3188,17 +3195,7 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
     };
     start(all, 1);
 
-    std::vector<RhsState> hs(kk);
-    int* flag = ctx->pinned_flag;
-    const int chunk = 32;
-    for (int restart_round = 0;; ++restart_round) {
-      // ---- iterate until no column is active ------------------------------
-      int polls_in_flight = 0;
-      cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
-      int launched = 0;
-      const int cap = opt.max_iter + chunk;  // iterations can never exceed max_iter
-      for (; opt.max_iter > 0;) {
-        for (int it = 0; it < chunk; ++it) {
+    auto iteration = [&]() {
           cudaEvent_t ev[2];
           prof_begin(ctx, ev, 0, true, n_active.p, k);
           DK::spmv(ctx, kCocg, grid_s, n, a, p.p, q.p, nullptr, ctl);
@@ -3227,6 +3224,61 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
             prof_end(ctx, ev2);
           }
           note_launch(ctx, 3);
+            };
+    // one iteration captured as a CUDA graph (multigrid path only: with Jacobi
+    // the iteration is 3 bandwidth-bound launches and a graph gives nothing),
+    // kept with the hierarchy across solves
+    IterGraph none;
+    IterGraph& graph = ext ? a->amg->iter : none;
+    if (ext && std::getenv("ECT_NO_GRAPH") == nullptr && !trace) {
+      const void* tag[3] = {r.p, partial.p, st.p};
+      const bool valid = graph.exec && graph.k == kk && graph.tol == opt.tol &&
+                         graph.max_iter == opt.max_iter && graph.tag[0] == tag[0] &&
+                         graph.tag[1] == tag[1] && graph.tag[2] == tag[2];
+      if (!valid) {
+        graph.reset();
+        const bool prof_was = ctx->prof.enabled;
+        ctx->prof.enabled = false;  // no event records inside the capture
+        const int64_t l0 = ctx->timings.kernel_launches;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        iteration();
+        CK(cudaStreamEndCapture(s, &graph.graph));
+        graph.launches = (int)(ctx->timings.kernel_launches - l0);
+        ctx->timings.kernel_launches = l0;  // captured, not launched
+        ctx->prof.enabled = prof_was;
+        CK(cudaGraphInstantiate(&graph.exec, graph.graph, 0));
+        graph.k = kk;
+        graph.tol = opt.tol;
+        graph.max_iter = opt.max_iter;
+        for (int q = 0; q < 3; ++q) graph.tag[q] = tag[q];
+      }
+    } else if (ext) {
+      graph.reset();
+    }
+
+    std::vector<RhsState> hs(kk);
+    int* flag = ctx->pinned_flag;
+    const int chunk = 32;
+    for (int restart_round = 0;; ++restart_round) {
+      // ---- iterate until no column is active ------------------------------
+      int polls_in_flight = 0;
+      cudaEvent_t poll_ev[2] = {ctx->ev_a, ctx->ev_b};
+      int launched = 0;
+      const int cap = opt.max_iter + chunk;  // iterations can never exceed max_iter
+      for (; opt.max_iter > 0;) {
+        for (int it = 0; it < chunk; ++it) {
+          // the multigrid iteration is ~46 launches, most of them 4-30 us
+          // coarse-level kernels: replayed as one CUDA graph (captured once per
+          // solve) the host enqueues 1 node list instead of 46 launches and
+          // stops being the bottleneck of the coarse part; profiled sample
+          // iterations go through the plain launches with their events
+          if (graph.exec && !prof_sample_next(ctx)) {
+            if (ctx->prof.enabled) ++ctx->prof.launches;  // keep the sampling stride
+            CK(cudaGraphLaunch(graph.exec, s));
+            note_launch(ctx, graph.launches);
+            continue;
+          }
+          iteration();
         }
         launched += chunk;
         CK(cudaMemcpyAsync(flag + (polls_in_flight & 1), n_active.p, sizeof(int),

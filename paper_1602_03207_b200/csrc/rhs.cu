@@ -285,9 +285,12 @@ void build_rhs(ect_mesh* m, const ect_coil& coil, const double* z, const int* wh
   cudaStream_t s = ctx->stream;
   const int64_t nn = m->n_nodes, N = 3 * nn + m->n_cond;
   CK(cudaMemsetAsync(rhs, 0, (size_t)N * n_rhs * sizeof(double2), s));
-  DevBuf<uint8_t> flag(nn);
-  DevBuf<double> j(3 * nn);
-  DevBuf<int> stat(2);
+  m->rhs_flag.ensure(nn);
+  m->rhs_j.ensure(3 * nn);
+  m->rhs_stat.ensure(4);
+  struct { uint8_t* p; size_t n; size_t bytes() const { return n; } } flag{m->rhs_flag.p, (size_t)nn};
+  struct { double* p; } j{m->rhs_j.p};
+  struct { int* p; } stat{m->rhs_stat.p};
   for (int col = 0; col < n_rhs; ++col) {
     if (which[col] != 1 && which[col] != 2) fail(ECT_ERR_MESH, "coil_support: coil index must be 1 or 2");
     const double lo = which[col] == 1 ? z[col] - 0.5 * coil.gap - coil.height : z[col] + 0.5 * coil.gap;
@@ -323,9 +326,12 @@ void build_rhs_support(ect_mesh* m, const int* support, int64_t n_support, int r
   cudaStream_t s = ctx->stream;
   const int64_t nn = m->n_nodes, N = 3 * nn + m->n_cond;
   CK(cudaMemsetAsync(rhs, 0, (size_t)N * sizeof(double2), s));
-  DevBuf<uint8_t> flag(nn);
-  DevBuf<double> j(3 * nn);
-  DevBuf<int> stat(3);
+  m->rhs_flag.ensure(nn);
+  m->rhs_j.ensure(3 * nn);
+  m->rhs_stat.ensure(4);
+  struct { uint8_t* p; size_t n; size_t bytes() const { return n; } } flag{m->rhs_flag.p, (size_t)nn};
+  struct { double* p; } j{m->rhs_j.p};
+  struct { int* p; } stat{m->rhs_stat.p};
   CK(cudaMemsetAsync(flag.p, 0, flag.bytes(), s));
   int init[3] = {0, 0x7fffffff, 0x7fffffff};
   CK(cudaMemcpyAsync(stat.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
@@ -379,7 +385,9 @@ void delta_impedance(ect_mesh* m, const ect_materials& pm, const ect_materials& 
     P.sigma_d[r] = pm.sigma[r];
     P.sigma_eps[r] = rm.sigma[r];
   }
-  DevBuf<double> contrib(8 * m->n_defect), res(8);
+  m->dz_contrib.ensure(8 * (size_t)std::max<int64_t>(1, m->n_defect));
+  m->dz_res.ensure(8);
+  struct { double* p; } contrib{m->dz_contrib.p}, res{m->dz_res.p};
   k_dz_contrib<<<blocks_for(ctx, m->n_defect, 128), 128, 0, s>>>(
       m->tets.p, m->region.p, m->xyz.p, m->defect_tets.p, m->n_defect, m->cond_fwd.p,
       3 * m->n_nodes, xk1, xk2, xl1, xl2, stride, P, contrib.p);
