@@ -1795,7 +1795,14 @@ struct Dispatch {
       default: return grid_for(ctx, csr_fn<K>(mode), kBlock);
     }
   }
-  static int vec_grid(ect_ctx* ctx) { return grid_for(ctx, (const void*)k_update<K>, kBlock); }
+  static int vec_grid(ect_ctx* ctx) {
+    static const int ctas = [] {  // dev: CTAs per SM of the vector kernels
+      const char* v = std::getenv("ECT_VEC_CTAS");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (ctas > 0) return ctas * ctx->num_sms;
+    return grid_for(ctx, (const void*)k_update<K>, kBlock);
+  }
 };
 
 // Runs fn with the Dispatch<K> matching k.
@@ -2753,6 +2760,9 @@ KFn nbe32_fn() {
   else if constexpr (K == 4) return {(const void*)k_nbe32<4, K, MODE, 3, 2>, kBlock};
   else if constexpr (K == 8) {  // 64 registers (32 warps/SM); the dot epilogue needs 73
     constexpr int MINB = MODE == kSmoothDot ? 7 : 8;
+    static const bool dot8 = std::getenv("ECT_F32_DOT_MINB8") != nullptr;  // dev A/B
+    if (MODE == kSmoothDot && dot8)
+      return {(const void*)k_nbe32<4, K, MODE, 8, 4, 128, true, 2>, 128};
     return {(const void*)k_nbe32<4, K, MODE, MINB, 4, 128, true, 2>, 128};
   } else return {(const void*)k_nbe32<8, K, MODE, 2, 8>, kBlock};
 }
