@@ -36,6 +36,31 @@ def test_reference_reader_accepts_our_trace(tmp_path, ref_lib):
     assert 0 < dev < 1e-8
 
 
+def test_configs3_golden_trace_is_consistent():
+    """tests/golden/trace_cfg3.csv (written by the reference's write_trace_csv)
+    against the generator's record trace_cfg3.json: the 8 documented configs[3]
+    positions, the same impedances to the CSV's 12 digits, modes = signal_modes
+    of the four DeltaZ (signals.cpp:101-107), and every reference solve's TRUE
+    residual recorded (the bar of the GPU curve test rests on them)."""
+    import json
+    rows = trace.read_trace_csv(GOLDEN / "trace_cfg3.csv")
+    doc = json.loads((GOLDEN / "trace_cfg3.json").read_text())
+    w = workloads.config3()
+    pts = sorted(doc["points"].items(), key=lambda kv: kv[1]["z"])
+    assert sorted(int(i) for i, _ in pts) == [0, 13, 20, 26, 31, 36, 45, 63]
+    assert len(rows) == len(pts)
+    for (z, sig), (i, p) in zip(rows, pts):
+        assert abs(z - w.positions[int(i)]) <= 1e-11 * abs(z)
+        dz = np.array([complex(*v) for v in p["dz"]])
+        modes = np.array([complex(*v) for v in p["modes"]])
+        ref = np.concatenate([dz, modes])
+        assert np.max(np.abs(np.array(sig) - ref)) <= 1e-11 * np.max(np.abs(ref))
+        assert abs(modes[0] - 0.5j * (dz[0] + dz[1])) <= 1e-14 * abs(dz[0])
+        assert abs(modes[1] - 0.5j * (dz[0] - dz[3])) <= 1e-14 * abs(dz[0])
+        assert len(p["true_residual"]) == 4 and max(p["true_residual"]) <= 5e-9
+    assert doc["worst_true_residual"] == max(max(p["true_residual"]) for _, p in pts)
+
+
 @pytest.mark.gpu
 def test_gpu_sweep_trace_matches_reference(ctx, tmp_path):
     g = golden("small_6x6x12")
