@@ -102,3 +102,33 @@ def test_profiled_launches_count_full_width_only(ctx, system):
     ctx.set_profiling(False)
     part = ctx.timings(reset=True)
     assert part["spmv_launches"] == 0 and part["spmv_partial_launches"] >= 40 // 8
+
+
+def test_multigrid_iteration_graph_is_recaptured(ctx):
+    """The multigrid COCG replays its iteration as a CUDA graph kept with the
+    hierarchy (krylov.cu cocg_solve, IterGraph): kernel arguments bake in the
+    batch width, the tolerance and max_iter. Alternating widths and stopping
+    parameters on one matrix must re-capture, i.e. give bitwise the solutions
+    of a fresh matrix solved once with the same parameters, and the plain
+    launches (ECT_NO_GRAPH has the same arithmetic) agree through the residual."""
+    from paper_1602_03207_b200 import workloads
+    from tests.helpers import ref_matrix
+    g = golden("small_6x6x12")
+    mesh = ect.Mesh(ctx, g["xyz"], g["tets"], g["region"])
+    p, _, _ = mesh.materials(workloads.Physics(sigma_defect=1e4, mu_r_defect=5.0))
+    A = ref_matrix(g, "primary").tocsr()
+    rng = np.random.default_rng(5)
+    n = A.shape[0]
+    b8 = rng.uniform(-1, 1, (n, 8)) + 1j * rng.uniform(-1, 1, (n, 8))
+    b2 = np.ascontiguousarray(b8[:, :2])
+    cases = [(b8, 1e-8, 500), (b2, 1e-10, 400), (b8, 1e-8, 500), (b8, 1e-6, 500), (b2, 1e-10, 400)]
+    a = ect.Matrix(ctx, mesh).assemble(p)  # multigrid is the default preconditioner
+    seq = [a.solve(b, tol=tol, max_iter=mi) for b, tol, mi in cases]
+    for (b, tol, mi), (x, res) in zip(cases, seq):
+        fresh = ect.Matrix(ctx, mesh).assemble(p)
+        xf, rf = fresh.solve(b, tol=tol, max_iter=mi)
+        assert [r["iterations"] for r in res] == [r["iterations"] for r in rf]
+        assert x.tobytes() == xf.tobytes()
+        assert all(r["converged"] for r in res)
+        rr = np.linalg.norm(b - A @ x, axis=0) / np.linalg.norm(b, axis=0)
+        assert np.all(rr <= tol * 1.01), rr
