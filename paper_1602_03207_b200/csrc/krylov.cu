@@ -1795,13 +1795,18 @@ struct Dispatch {
       default: return grid_for(ctx, csr_fn<K>(mode), kBlock);
     }
   }
-  static int vec_grid(ect_ctx* ctx) {
-    static const int ctas = [] {  // dev: CTAs per SM of the vector kernels
-      const char* v = std::getenv("ECT_VEC_CTAS");
-      return v ? std::atoi(v) : 0;
-    }();
-    if (ctas > 0) return ctas * ctx->num_sms;
-    return grid_for(ctx, (const void*)k_update<K>, kBlock);
+  // Grid of the fused vector kernels. Multigrid path (ext): k_update / k_pupdate
+  // hold 48 registers, and 4 CTAs per SM run them at 0.15 ms instead of 0.18 ms
+  // (k = 8, r02 bench A/B); the Jacobi kernels (100 registers) keep their
+  // occupancy-sized grid, where more CTAs measured no gain.
+  static int vec_grid(ect_ctx* ctx, bool ext = false) {
+    const int base = grid_for(ctx, (const void*)k_update<K>, kBlock);
+    if (!ext) return base;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<K, true>, kBlock, 0));
+    int per_p = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_p, k_pupdate<K, true>, kBlock, 0));
+    return std::max(base, std::min({4, per_sm, per_p}) * ctx->num_sms);
   }
 };
 
@@ -2759,10 +2764,8 @@ KFn nbe32_fn() {
   if constexpr (K <= 2) return {(const void*)k_nbe32<2, K, MODE, 3, 1>, kBlock};
   else if constexpr (K == 4) return {(const void*)k_nbe32<4, K, MODE, 3, 2>, kBlock};
   else if constexpr (K == 8) {  // 64 registers (32 warps/SM); the dot epilogue needs 73
+    // (forced to 64 it spills and the iteration is 1.7% slower)
     constexpr int MINB = MODE == kSmoothDot ? 7 : 8;
-    static const bool dot8 = std::getenv("ECT_F32_DOT_MINB8") != nullptr;  // dev A/B
-    if (MODE == kSmoothDot && dot8)
-      return {(const void*)k_nbe32<4, K, MODE, 8, 4, 128, true, 2>, 128};
     return {(const void*)k_nbe32<4, K, MODE, MINB, 4, 128, true, 2>, 128};
   } else return {(const void*)k_nbe32<8, K, MODE, 2, 8>, kBlock};
 }
@@ -3147,7 +3150,7 @@ void cocg_solve(ect_ctx* ctx, ect_matrix* a, const double2* b, double2* x, int k
     constexpr int KW = DK::kWidth;
     const int grid_s = DK::spmv_grid(ctx, kCocg, a);
     const int grid_r = DK::spmv_grid(ctx, kResid, a);
-    const int grid_v = DK::vec_grid(ctx);
+    const int grid_v = DK::vec_grid(ctx, ext);
     std::unique_ptr<Cycle<KW>> cyc;
     if (ext) cyc = std::make_unique<Cycle<KW>>(ctx, a, *a->amg);
     const int grid_max = std::max({grid_s, grid_r, grid_v, cyc ? cyc->max_grid() : 0});

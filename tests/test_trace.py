@@ -57,7 +57,7 @@ def test_configs3_golden_trace_is_consistent():
         assert np.max(np.abs(np.array(sig) - ref)) <= 1e-11 * np.max(np.abs(ref))
         assert abs(modes[0] - 0.5j * (dz[0] + dz[1])) <= 1e-14 * abs(dz[0])
         assert abs(modes[1] - 0.5j * (dz[0] - dz[3])) <= 1e-14 * abs(dz[0])
-        assert len(p["true_residual"]) == 4 and max(p["true_residual"]) <= 5e-9
+        assert len(p["true_residual"]) == 4 and max(p["true_residual"]) <= 1.01e-10
     assert doc["worst_true_residual"] == max(max(p["true_residual"]) for _, p in pts)
 
 
@@ -82,16 +82,17 @@ def test_gpu_configs3_sweep_matches_reference_trace(ctx, tmp_path):
     (4 per matrix pass) against the reference's own run_scan chain at the same
     positions (tests/golden/trace_cfg3.csv: 8 of the 64 -- both far-field
     ends, both deposit edges, the centre and three fill positions -- solved by
-    the reference's stock GMRES(80)+ILU(0) asked for 1e-10 on the GPU box's 16
-    host cores, oracle/make_golden.py cfg3_trace_batched: the reference
-    configuration's solves reach 1e-10 in 640-712 iterations, the primary
-    configuration's stall and were stopped at 1,500 iterations with TRUE
-    residuals 2.9e-10 .. 3.3e-9, all recorded in trace_cfg3.json). The GPU
-    solves to 1e-12 so the bar is not spent on our own convergence error. Bar per
-    signal over the curve: max_z |S(z) - S*(z)| / max |DeltaZ*| <= 1e-6
-    (SURVEY §8(c) impedance metric); each signal against its own curve
-    maximum and the reference's per-point max_relative_deviation
-    (scan.cpp:252-272) are reported beside it."""
+    the reference's solve_iterative, GMRES(restart 240)+ILU(0) to 1e-10, on
+    the GPU box's 16 host cores, oracle/make_golden.py cfg3_trace_batched:
+    689-762 iterations per primary-configuration solve, 464-503 per
+    reference-configuration solve, every TRUE residual <= 1e-10 and recorded in
+    trace_cfg3.json; with the stock restart of 80 the primary solves stall near
+    3e-9, profiles/r02_cfg3_trace_gmres80_stalled.json). The GPU solves to
+    1e-12 so the bar is not spent on our own convergence error. Bar per
+    signal over the curve, each against its own curve maximum:
+    max_z |S(z) - S*(z)| / max_z |S*(z)| <= 1e-6; the SURVEY 8(c) figure
+    (normalised by max |DeltaZ*|) and the reference's per-point
+    max_relative_deviation (scan.cpp:252-272) are reported beside it."""
     gold_path = GOLDEN / "trace_cfg3.csv"
     if not gold_path.exists():
         pytest.skip("trace_cfg3.csv not generated (python -m oracle.make_golden cfg3_trace_batched)")
@@ -122,10 +123,9 @@ def test_gpu_configs3_sweep_matches_reference_trace(ctx, tmp_path):
           " ".join(f"{v:.2e}" for v in own),
           f"; per-point max_relative_deviation {trace.max_relative_deviation(gold, ours):.2e}")
     assert np.all(dev <= 1e-6), dev
-    # Z_F3 = (i/2)(Z11 - Z22) is a difference of nearly equal impedances: on its
-    # own (5x smaller) scale the reference's convergence error (true residuals up
-    # to 3.3e-9 in the primary configuration, trace_cfg3.json) shows as ~4e-6
-    assert np.all(own[:5] <= 1e-6) and own[5] <= 1e-5, own
+    # also on every signal's own scale (Z_F3 = (i/2)(Z11 - Z22), a difference of
+    # nearly equal impedances, is 5x smaller than DeltaZ)
+    assert np.all(own <= 1e-6), own
 
 
 @pytest.mark.gpu
