@@ -1667,7 +1667,10 @@ KFn nbe_kernel() {
   else if constexpr (K == 4) return {(const void*)k_nbe_spmv<2, K, MODE, 2, 2, 4>, kBlock};
   else if constexpr (K == 8)  // flat loop, 2 columns per lane (lab: 0.282 vs 0.327 ms)
     return {(const void*)k_nbe_spmv<4, K, MODE, 2, 4, 2, kBlock, true>, kBlock};
-  else return {(const void*)k_nbe_spmv<8, K, MODE, 2, 8>, kBlock};
+  else {
+    if constexpr (MODE == kCgDot) return {(const void*)k_nbe_spmv<8, K, MODE, 2, 8>, kBlock};
+    else return {(const void*)k_nbe_spmv<8, K, MODE, 2, 8, 2, kBlock, true>, kBlock};
+  }
 }
 template <int K>
 KFn nbe_fn(int mode) {
@@ -2767,7 +2770,10 @@ KFn nbe32_fn() {
     // (forced to 64 it spills and the iteration is 1.7% slower)
     constexpr int MINB = MODE == kSmoothDot ? 7 : 8;
     return {(const void*)k_nbe32<4, K, MODE, MINB, 4, 128, true, 2>, 128};
-  } else return {(const void*)k_nbe32<8, K, MODE, 2, 8>, kBlock};
+  } else {
+    constexpr int MINB = MODE == kSmoothDot ? 7 : 8;
+    return {(const void*)k_nbe32<8, K, MODE, MINB, 8, 128, true, 2>, 128};
+  }
 }
 
 __global__ void k_to_f32(const double* __restrict__ a, int64_t n, float* __restrict__ out) {
