@@ -2767,7 +2767,8 @@ KFn nbe32_fn() {
   if constexpr (K <= 2) return {(const void*)k_nbe32<2, K, MODE, 3, 1>, kBlock};
   else if constexpr (K == 4) return {(const void*)k_nbe32<4, K, MODE, 3, 2>, kBlock};
   else if constexpr (K == 8) {  // 64 registers (32 warps/SM); the dot epilogue needs 73
-    // (forced to 64 it spills and the iteration is 1.7% slower)
+    // (forced to 64 registers it spills and the iteration is 1.7% slower; at 85
+    // registers / 24 warps it is 0.3% slower)
     constexpr int MINB = MODE == kSmoothDot ? 7 : 8;
     return {(const void*)k_nbe32<4, K, MODE, MINB, 4, 128, true, 2>, 128};
   } else {
